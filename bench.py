@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: FP64 DOF-updates/s of the MRAB + PP + TVB nodal-DG
+shallow-water step at N = 3 on the synthetic C5 tsunami basin.
+
+One "step" = one MRAB macro step (2^(L-1) finest substeps, every level updated
+its 2^(L-l) times, K1 + K2 per update).  DOF-update = (element, node, field)
+advanced by one substep of its level: U = 3 Np sum_l K_l 2^(L-l) per macro step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle
+(the deliberately slow checker) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "DOF-updates/s (FP64, N=3) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "DOF-updates/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def workload(P_strip: int, base_n: int, strip: int = 1):
+    import swe_inputs as si
+    return si.c5_tsunami(P=P_strip, base_n=base_n, strip=strip)
+
+
+def dof_per_macro_step(levels: np.ndarray, L: int, Np: int) -> int:
+    cnt = np.bincount(levels, minlength=L + 1)
+    return int(3 * Np * sum(int(cnt[l]) * 2 ** (L - l) for l in range(1, L + 1)))
+
+
+def cpu_baseline(args, seconds_budget=30.0):
+    """The oracle as it stands, on a bounded sample: a y-strip of the C5 mesh, 1 macro step."""
+    import oracle
+    import swe_inputs as si
+    cores = oracle.set_threads(0)
+    w = workload(1, args.base_n, strip=args.cpu_strip)
+    m = w.mesh
+    Np = 10
+    probe = oracle.Oracle(m.vx, m.vy, m.etov, np.zeros((m.K, Np)), 3, w.g, **w.params)
+    x, y = probe.nodes()
+    del probe
+    B, h, hu, hv = w.fields(x, y)
+    o = oracle.Oracle(m.vx, m.vy, m.etov, B, 3, w.g, **w.params)
+    o.set_state(h, hu, hv)
+    dt = si.dt_for(m, 3, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
+    o.step(dt, w.nlevels)  # schedule + first (Euler) step, untimed
+    lev = o.levels()
+    U = dof_per_macro_step(lev, w.nlevels, Np)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        rc = o.step(dt, w.nlevels)
+        assert rc == 0
+        n += 1
+        if time.perf_counter() - t0 > seconds_budget * 0.5 or n >= args.cpu_steps:
+            break
+    el = time.perf_counter() - t0
+    return {"value": U * n / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"C5 y-strip 1/{args.cpu_strip} ({m.K} elements, N=3, L={w.nlevels}), {n} macro step(s) after "
+                      f"the first, {el:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle timed as it stands on the box's host cores."""
+    if rank != 0:
+        return
+    import oracle
+    import swe_inputs as si
+    cores = oracle.set_threads(0)
+    w = workload(1, args.base_n, strip=args.cpu_strip)
+    m = w.mesh
+    Np = 10
+    probe = oracle.Oracle(m.vx, m.vy, m.etov, np.zeros((m.K, Np)), 3, w.g, **w.params)
+    x, y = probe.nodes()
+    del probe
+    B, h, hu, hv = w.fields(x, y)
+    o = oracle.Oracle(m.vx, m.vy, m.etov, B, 3, w.g, **w.params)
+    o.set_state(h, hu, hv)
+    dt = si.dt_for(m, 3, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
+    for _ in range(args.warmup):
+        assert o.step(dt, w.nlevels) == 0
+    lev = o.levels()
+    U = dof_per_macro_step(lev, w.nlevels, Np)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        assert o.step(dt, w.nlevels) == 0
+    el = time.perf_counter() - t0
+    val = U * args.steps / el
+    sample = f"C5 y-strip 1/{args.cpu_strip} ({m.K} elements, N=3, L={w.nlevels})"
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": sample, "N": 3, "nlevels": w.nlevels},
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--base-n", type=int, default=1280)
+    ap.add_argument("--cpu-strip", type=int, default=32)
+    ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert args.warmup >= 3 or args.impl == "reference", "W >= 3"
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    import paper_1403_1661_b200 as P
+    import swe_inputs as si
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P.lib()
+
+    # ---- workload (C5, weak scaling: each rank owns a 2000 km x 2000 km basin strip of the P-wide domain)
+    t_setup = time.time()
+    w = workload(1, args.base_n)
+    m = w.mesh
+    N, Np, L = 3, 10, w.nlevels
+    x, y = P.nodes(m.vx, m.vy, m.etov, N)
+    B, h, hu, hv = w.fields(x, y)
+    del x, y
+    s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=w.params, device=local)
+    dt = si.dt_for(m, N, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
+    s.set_state(h, hu, hv)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        s.step(dt, L)
+    lev = s.levels()
+    U = dof_per_macro_step(lev, L, Np)
+    t_setup = time.time() - t_setup
+
+    # ---- timed region: K macro steps, device time with CUDA events on the solver's stream
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    s.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            s.step(dt, L)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    s.profile(False)
+    ms = ev0.elapsed_time(ev1)
+    prof = s.profile_read()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    ms_per_step = ms / args.steps
+    value = U * world * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (K1), algorithmic bytes / event-timed launch duration
+    peak, peak_kind = load_peaks()
+    k1_gbs = prof["k1_bytes"] / (prof["k1_ms"] / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
+            "traffic": None, "kernel": "k_rhs_update<3>", "peak_kind": peak_kind,
+            "k1_share_of_step": prof["k1_ms"] / ms if ms > 0 else None,
+            "k2_share_of_step": prof["k2_ms"] / ms if ms > 0 else None}
+    traffic_path = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
+    if os.path.exists(traffic_path):
+        try:
+            roof["traffic"] = json.load(open(traffic_path)).get("bytes_per_launch_per_elem_update")
+        except Exception:
+            pass
+
+    info = s.info()
+
+    # ---- end to end through the C ABI with host buffers (H2D of the state, D2H of the result every step)
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+        hh, hhu, hhv = pin(h), pin(hu), pin(hv)
+        oh, ohu, ohv = pin(np.zeros_like(h)), pin(np.zeros_like(h)), pin(np.zeros_like(h))
+        s2 = s
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2.set_state(hh, hhu, hhv)
+        for _ in range(args.e2e_steps):
+            s2.step(dt, L)
+            s2.get_state_into(oh, ohu, ohv)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        state_bytes = 3 * h.size * 8
+        e2e = {"value": U * world * args.e2e_steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(state_bytes / args.e2e_steps), "d2h_bytes_per_step": int(state_bytes),
+               "note": "set_state (H2D, incl. level binning + initial limiting) once, then per macro step swe_step + "
+                       "swe_get_state (D2H) into pinned host buffers; wall clock"}
+
+    s.close()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args)
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5 synthetic tsunami basin (SURVEY 8(d)), N=3, 4 MRAB levels, PP+TVB",
+                       "K": int(m.K), "level_counts": [int(c) for c in np.bincount(lev, minlength=L + 1)[1:]],
+                       "dof_updates_per_step": U, "dt": dt, "l2": "inputs larger than L2 (state+history ~13 GB)",
+                       "setup_s": round(t_setup, 1)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(prof["k1_launches"] + prof["k2_launches"]),
+            "clocks": clk.summary(),
+            "counters": {"n_pp": info["n_pp"], "n_dry": info["n_dry"], "n_tvb": info["n_tvb"]},
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

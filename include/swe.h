@@ -1,0 +1,160 @@
+/* include/swe.h -- C ABI of the B200-native DG shallow-water solver.
+ *
+ * Implements the data-parallel hot path of arXiv:1403.1661 (PAPER.md, cited
+ * as P:n = line n): the nodal discontinuous-Galerkin right-hand side of the
+ * 2D shallow water equations on unstructured triangles (Eqs. 1-6:
+ * volume term N(Q) = Pr cF1 + Ps cF2 + P cS; surface term
+ * S = -L^g F*_n; well-balanced Lax-Friedrichs flux),
+ * advanced by multi-rate Adams-Bashforth local time stepping (P:115-147,
+ * Alg. 1) with the positivity-preserving limiter M Pi (Alg. 3) and
+ * the TVB limiter Lambda Pi after every update (Alg. 2).
+ * The readings of the paper that this library implements are listed in
+ * DESIGN.md ("Readings").
+ *
+ * Conventions (all calls):
+ *   - Every pointer argument is HOST memory owned by the caller.  Inputs are
+ *     copied during the call and never retained; outputs are written before
+ *     the call returns.
+ *   - Nodal arrays are [element][node] in the caller's element order, node
+ *     order = Hesthaven-Warburton Nodes2D of the element AFTER the orientation
+ *     fix (rows of constant s from s = -1 upward, r increasing in a row;
+ *     N = 2: (-1,-1),(0,-1),(1,-1),(-1,0),(0,0),(-1,1)), reference triangle
+ *     (-1,-1),(1,-1),(-1,1), face f runs vertex f -> vertex (f+1)%3.
+ *     swe_nodes() returns the physical coordinates of those nodes.
+ *   - Clockwise triangles are re-oriented by swapping their 2nd and 3rd
+ *     vertex (counted in swe_info.nflipped).
+ *   - Errors are negative return codes; nothing aborts.  The message of the
+ *     last error of a context is available from swe_last_error().
+ *   - A context is not thread-safe; distinct contexts are independent.
+ *   - Arithmetic is IEEE binary64 throughout (device and host).
+ */
+#ifndef SWE_H
+#define SWE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SWE_OK = 0,
+  SWE_ERR_ARG = -1,       /* invalid argument (NULL, size, dt <= 0, nlevels out of [1,8]) */
+  SWE_ERR_MESH = -2,      /* vertex index out of range, zero-area element, face with > 2 owners */
+  SWE_ERR_ORDER = -3,     /* polynomial order outside the supported range [1, 4] */
+  SWE_ERR_STATE = -4,     /* swe_step / swe_get_state before swe_set_state */
+  SWE_ERR_SCHEDULE = -5,  /* (dt, nlevels) differ from the first swe_step after swe_set_state */
+  SWE_ERR_NONFINITE = -6, /* NaN/Inf produced; the state is left as computed */
+  SWE_ERR_CUDA = -7,      /* CUDA runtime error, or no device */
+  SWE_ERR_NCCL = -8,      /* reserved for the multi-GPU exchange */
+  SWE_ERR_NOMEM = -9      /* device allocation failed */
+};
+
+typedef struct swe_ctx swe_ctx;
+
+/* Conforming triangulation.  Faces are matched on the sorted pair of
+ * canonical vertex ids vperiodic[v] (identity when NULL), which is how
+ * periodic partners are expressed.  Unmatched faces are reflective walls. */
+typedef struct {
+  int32_t nverts;
+  const double *vx, *vy;      /* [nverts] */
+  int32_t nelems;
+  const int32_t *etov;        /* [nelems*3], 0-based vertex indices */
+  const int32_t *vperiodic;   /* [nverts] or NULL */
+} swe_mesh;
+
+/* Parameters; a zero-initialised struct (or NULL) selects the defaults. */
+typedef struct {
+  double h0;       /* dry threshold of Alg. 3, default 1e-6 */
+  double eps;      /* Alg. 3 trigger: limit when min nodal h <= eps, default h0 */
+  double tvb_M;    /* TVB constant M, threshold M*Hk^2 (default 0 = TVD minmod) */
+  double tvb_nu;   /* Cockburn-Shu nu, default 1.5 */
+  double a_floor;  /* lower bound of the wave speed used for level binning, default 0 */
+  double eps_u;    /* velocity desingularisation scale, default 1000*h0 (A4') */
+  double h_char;   /* below this mean depth TVB limits component-wise, default 10*h0 */
+  int32_t use_pp;  /* apply M Pi (Alg. 3); default 0 when the struct is zero -- set 1 to enable */
+  int32_t use_tvb; /* apply Lambda Pi */
+  int32_t device;  /* CUDA device ordinal */
+  void *stream;    /* cudaStream_t for all work (e.g. torch.cuda.current_stream()), NULL = legacy default */
+  /* optional device allocator (e.g. the torch caching allocator); NULL => cudaMalloc/cudaFree */
+  void *(*dev_alloc)(size_t bytes, void *stream, void *user);
+  void (*dev_free)(void *ptr, void *stream, void *user);
+  void *alloc_user;
+} swe_params;
+
+typedef struct {
+  double t;              /* simulated time (sum of macro steps) */
+  double mass;           /* sum_e J_e int h (current state) */
+  double injected_mass;  /* mass added by the dry branch of Alg. 3 since swe_set_state */
+  double min_h;          /* minimum nodal h */
+  int64_t n_pp;          /* Alg. 3 triggers (h_min <= eps) */
+  int64_t n_dry;         /* Alg. 3 dry-branch applications */
+  int64_t n_tvb;         /* elements replaced by the TVB limiter */
+  int64_t n_updates;     /* element updates (sum over launched levels) */
+  int32_t K, Np, N, nlevels, nflipped;
+  int32_t level_count[8];
+} swe_info;
+
+/* ------------------------------------------------------------ solver */
+
+/* Physical coordinates of the nodes of every element, [nelems*Np] each.
+ * Host only (no device needed).  Returns SWE_OK or SWE_ERR_MESH/ORDER/ARG. */
+int swe_nodes(const swe_mesh *mesh, int N, double *x, double *y);
+
+/* Build a solver for order N in [1,4], gravity g > 0, nodal bathymetry B
+ * ([nelems*Np], P^N per element).  Host builder (reference element, mesh
+ * connectivity, geometry) + device upload.  On failure *out = NULL. */
+int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe_params *params,
+               swe_ctx **out);
+
+/* Set the nodal state (h, hu, hv), each [nelems*Np].  Resets time, the AB
+ * start-up ramp, the counters and the level schedule; the limiters of Alg. 2
+ * line 1 (Q^0 = Lambda Pi M Pi Q^0) are applied lazily by the next
+ * swe_step / swe_get_state.  Levels are binned from this unlimited state. */
+int swe_set_state(swe_ctx *ctx, const double *h, const double *hu, const double *hv);
+
+/* One MRAB macro step of length 2^(nlevels-1)*dt (level l steps with
+ * 2^(l-1) dt; dt is the finest level's step).  The first call after
+ * swe_set_state bins the levels (Eq. cfl) and fixes them for the
+ * run; later calls with another (dt, nlevels) fail with
+ * SWE_ERR_SCHEDULE.  Synchronises the stream once to check for NaN/Inf. */
+int swe_step(swe_ctx *ctx, double dt, int nlevels);
+
+/* Copy the current state to the host, caller order, [nelems*Np] each. */
+int swe_get_state(swe_ctx *ctx, double *h, double *hu, double *hv);
+
+void swe_destroy(swe_ctx *ctx); /* NULL-safe; frees all device memory */
+
+/* ------------------------------------------------------------ introspection */
+int swe_get_levels(swe_ctx *ctx, int32_t *level);                       /* [nelems], 1..nlevels */
+int swe_get_connectivity(const swe_ctx *ctx, int32_t *etoe, int8_t *etof); /* [nelems*3], boundary = self */
+int swe_get_info(swe_ctx *ctx, swe_info *info);
+const char *swe_last_error(const swe_ctx *ctx);
+
+/* Per-kernel device time accumulated with CUDA events on the context stream
+ * while profiling is on: times_ms[0] = K1 (RHS + AB update + PP), [1] = K2
+ * (TVB); launches[] likewise; bytes[] = algorithmic bytes moved (DESIGN.md
+ * roofline model).  swe_profile(ctx, 1) resets and starts, 0 stops. */
+int swe_profile(swe_ctx *ctx, int on);
+int swe_profile_read(swe_ctx *ctx, double *times_ms, int64_t *launches, double *bytes);
+
+/* ------------------------------------------------------------ host-only builders (no device) */
+/* Reference-element operator by name ("r","s","Dr","Ds","Mref","Ic","Ig","P","Pr","Ps","Lg",
+ * "rc","sc","wc","tg","wg","wmean","Pv","Ig1"); rows/cols receive the shape, out may be NULL. */
+int swe_host_refel(int N, const char *name, double *out, int32_t *rows, int32_t *cols);
+/* Connectivity of a mesh exactly as swe_create builds it. */
+int swe_host_connectivity(const swe_mesh *mesh, int32_t *etoe, int8_t *etof, int32_t *nflipped);
+/* Element characteristic length Hk = 4A / perimeter (incircle diameter). */
+int swe_host_hk(const swe_mesh *mesh, double *hk);
+/* Level binning of a nodal state exactly as the first swe_step does it. */
+int swe_host_levels(const swe_mesh *mesh, int N, double g, const double *h, const double *hu, const double *hv,
+                    const swe_params *params, int nlevels, int32_t *level);
+/* Static TVB geometry: pairs[K*3*2] (neighbour face slots used for edge i), alphas[K*3*2]. */
+int swe_host_tvb_geometry(const swe_mesh *mesh, int32_t *pairs, double *alphas);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SWE_H */

@@ -1,0 +1,294 @@
+"""paper_1403_1661_b200 -- B200-native nodal-DG shallow-water solver (arXiv:1403.1661).
+
+Thin ctypes binding of the C ABI in include/swe.h (argument marshalling only:
+every step of the hot path runs in the sm_100a kernels of libswe_b200.so).
+PyTorch supplies the device memory (caching allocator) and the stream.
+There is no CPU fallback: if the extension is missing the import of
+``lib()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libswe_b200.so")
+
+SWE_ERRORS = {0: "SWE_OK", -1: "SWE_ERR_ARG", -2: "SWE_ERR_MESH", -3: "SWE_ERR_ORDER", -4: "SWE_ERR_STATE",
+              -5: "SWE_ERR_SCHEDULE", -6: "SWE_ERR_NONFINITE", -7: "SWE_ERR_CUDA", -8: "SWE_ERR_NCCL",
+              -9: "SWE_ERR_NOMEM"}
+
+EXPORTED = ["swe_nodes", "swe_create", "swe_set_state", "swe_step", "swe_get_state", "swe_destroy", "swe_get_levels",
+            "swe_get_connectivity", "swe_get_info", "swe_last_error", "swe_profile", "swe_profile_read",
+            "swe_host_refel", "swe_host_connectivity", "swe_host_hk", "swe_host_levels", "swe_host_tvb_geometry"]
+
+
+class SweError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"{SWE_ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class SweMesh(C.Structure):
+    _fields_ = [("nverts", C.c_int32), ("vx", C.POINTER(C.c_double)), ("vy", C.POINTER(C.c_double)),
+                ("nelems", C.c_int32), ("etov", C.POINTER(C.c_int32)), ("vperiodic", C.POINTER(C.c_int32))]
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class SweParams(C.Structure):
+    _fields_ = [("h0", C.c_double), ("eps", C.c_double), ("tvb_M", C.c_double), ("tvb_nu", C.c_double),
+                ("a_floor", C.c_double), ("eps_u", C.c_double), ("h_char", C.c_double),
+                ("use_pp", C.c_int32), ("use_tvb", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
+                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", C.c_void_p)]
+
+
+class SweInfo(C.Structure):
+    _fields_ = [("t", C.c_double), ("mass", C.c_double), ("injected_mass", C.c_double), ("min_h", C.c_double),
+                ("n_pp", C.c_int64), ("n_dry", C.c_int64), ("n_tvb", C.c_int64), ("n_updates", C.c_int64),
+                ("K", C.c_int32), ("Np", C.c_int32), ("N", C.c_int32), ("nlevels", C.c_int32),
+                ("nflipped", C.c_int32), ("level_count", C.c_int32 * 8)]
+
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    from . import buildlib as _b
+    return _b.build(force=force)
+
+
+def lib():
+    """Load libswe_b200.so (fails loudly when it is missing: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run python -m paper_1403_1661_b200.build")
+        L = C.CDLL(LIB_PATH)
+        dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+        vp = C.c_void_p
+        L.swe_nodes.argtypes = [C.POINTER(SweMesh), C.c_int, dp, dp]
+        L.swe_create.argtypes = [C.POINTER(SweMesh), dp, C.c_int, C.c_double, C.POINTER(SweParams), C.POINTER(vp)]
+        L.swe_set_state.argtypes = [vp, dp, dp, dp]
+        L.swe_step.argtypes = [vp, C.c_double, C.c_int]
+        L.swe_get_state.argtypes = [vp, dp, dp, dp]
+        L.swe_destroy.argtypes = [vp]
+        L.swe_destroy.restype = None
+        L.swe_get_levels.argtypes = [vp, ip]
+        L.swe_get_connectivity.argtypes = [vp, ip, C.POINTER(C.c_int8)]
+        L.swe_get_info.argtypes = [vp, C.POINTER(SweInfo)]
+        L.swe_last_error.argtypes = [vp]
+        L.swe_last_error.restype = C.c_char_p
+        L.swe_profile.argtypes = [vp, C.c_int]
+        L.swe_profile_read.argtypes = [vp, dp, C.POINTER(C.c_int64), dp]
+        L.swe_host_refel.argtypes = [C.c_int, C.c_char_p, dp, ip, ip]
+        L.swe_host_connectivity.argtypes = [C.POINTER(SweMesh), ip, C.POINTER(C.c_int8), ip]
+        L.swe_host_hk.argtypes = [C.POINTER(SweMesh), dp]
+        L.swe_host_levels.argtypes = [C.POINTER(SweMesh), C.c_int, C.c_double, dp, dp, dp, C.POINTER(SweParams),
+                                      C.c_int, ip]
+        L.swe_host_tvb_geometry.argtypes = [C.POINTER(SweMesh), ip, dp]
+        for n in EXPORTED:
+            if n not in ("swe_destroy", "swe_last_error"):
+                getattr(L, n).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _d(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a, t=C.c_double):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class _MeshArgs:
+    """Keeps the numpy buffers of a swe_mesh alive."""
+
+    def __init__(self, vx, vy, etov, vper=None):
+        self.vx, self.vy = _d(vx), _d(vy)
+        self.etov = np.ascontiguousarray(etov, dtype=np.int32).reshape(-1, 3)
+        self.vper = None if vper is None else np.ascontiguousarray(vper, dtype=np.int32)
+        self.K = self.etov.shape[0]
+        self.s = SweMesh(len(self.vx), _p(self.vx), _p(self.vy), self.K, _p(self.etov, C.c_int32),
+                         _p(self.vper, C.c_int32) if self.vper is not None else C.POINTER(C.c_int32)())
+
+
+def _check(rc, ctx=None):
+    if rc != 0:
+        msg = lib().swe_last_error(ctx).decode() if ctx else ""
+        raise SweError(rc, msg)
+
+
+def _params(p: dict | None, device=0, stream=None, alloc=None) -> SweParams:
+    p = dict(p or {})
+    sp = SweParams()
+    for k in ("h0", "eps", "tvb_M", "tvb_nu", "a_floor", "eps_u", "h_char"):
+        setattr(sp, k, float(p.get(k, 0.0)))
+    sp.use_pp = int(p.get("use_pp", 1))
+    sp.use_tvb = int(p.get("use_tvb", 1))
+    sp.device = int(device)
+    sp.stream = stream
+    if alloc is not None:
+        sp.dev_alloc, sp.dev_free = alloc
+    return sp
+
+
+def nodes(vx, vy, etov, N, vper=None):
+    """Physical node coordinates [K, Np] (x, y) in the library's node order (host only)."""
+    m = _MeshArgs(vx, vy, etov, vper)
+    Np = (N + 1) * (N + 2) // 2
+    x = np.zeros((m.K, Np))
+    y = np.zeros((m.K, Np))
+    _check(lib().swe_nodes(C.byref(m.s), N, _p(x), _p(y)))
+    return x, y
+
+
+def host_refel(N, name):
+    r, c = C.c_int32(), C.c_int32()
+    _check(lib().swe_host_refel(N, name.encode(), None, C.byref(r), C.byref(c)))
+    out = np.zeros((r.value, c.value))
+    _check(lib().swe_host_refel(N, name.encode(), _p(out), C.byref(r), C.byref(c)))
+    return out[:, 0] if c.value == 1 else out
+
+
+def host_connectivity(vx, vy, etov, vper=None):
+    m = _MeshArgs(vx, vy, etov, vper)
+    e = np.zeros((m.K, 3), dtype=np.int32)
+    f = np.zeros((m.K, 3), dtype=np.int8)
+    nf = C.c_int32()
+    _check(lib().swe_host_connectivity(C.byref(m.s), _p(e, C.c_int32), _p(f, C.c_int8), C.byref(nf)))
+    return e, f, nf.value
+
+
+def host_hk(vx, vy, etov, vper=None):
+    m = _MeshArgs(vx, vy, etov, vper)
+    hk = np.zeros(m.K)
+    _check(lib().swe_host_hk(C.byref(m.s), _p(hk)))
+    return hk
+
+
+def host_levels(vx, vy, etov, N, g, h, hu, hv, nlevels, params=None, vper=None):
+    m = _MeshArgs(vx, vy, etov, vper)
+    lev = np.zeros(m.K, dtype=np.int32)
+    h, hu, hv = _d(h), _d(hu), _d(hv)
+    sp = _params(params)
+    _check(lib().swe_host_levels(C.byref(m.s), N, float(g), _p(h), _p(hu), _p(hv), C.byref(sp), int(nlevels),
+                                 _p(lev, C.c_int32)))
+    return lev
+
+
+def host_tvb_geometry(vx, vy, etov, vper=None):
+    m = _MeshArgs(vx, vy, etov, vper)
+    pairs = np.zeros((m.K, 3, 2), dtype=np.int32)
+    al = np.zeros((m.K, 3, 2))
+    _check(lib().swe_host_tvb_geometry(C.byref(m.s), _p(pairs, C.c_int32), _p(al)))
+    return pairs, al
+
+
+class _TorchAllocator:
+    """Device memory from the torch caching allocator (PyTorch is plumbing only)."""
+
+    def __init__(self, device):
+        import torch
+        self.torch = torch
+        self.device = device
+
+        def _alloc(nbytes, stream, user):
+            return int(torch.cuda.caching_allocator_alloc(int(nbytes), self.device, stream))
+
+        def _free(ptr, stream, user):
+            torch.cuda.caching_allocator_delete(ptr)
+
+        self.alloc = ALLOC_FN(_alloc)
+        self.free = FREE_FN(_free)
+
+
+class Solver:
+    """One solver context (swe_create ... swe_destroy)."""
+
+    def __init__(self, vx, vy, etov, B, N, g, vper=None, params: dict | None = None, device: int = 0,
+                 use_torch: bool = True):
+        L = lib()
+        self._mesh = _MeshArgs(vx, vy, etov, vper)
+        self.K = self._mesh.K
+        self.N = N
+        self.Np = (N + 1) * (N + 2) // 2
+        self._B = _d(B).reshape(self.K, self.Np)
+        stream = None
+        self._alloc = None
+        if use_torch:
+            import torch
+            torch.cuda.set_device(device)
+            stream = C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+            self._alloc = _TorchAllocator(device)
+        self._sp = _params(params, device, stream,
+                           None if self._alloc is None else (self._alloc.alloc, self._alloc.free))
+        h = C.c_void_p()
+        rc = L.swe_create(C.byref(self._mesh.s), _p(self._B), N, float(g), C.byref(self._sp), C.byref(h))
+        if rc != 0:
+            raise SweError(rc, "swe_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().swe_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _shape(self, a):
+        return _d(a).reshape(self.K, self.Np)
+
+    def set_state(self, h, hu, hv):
+        h, hu, hv = self._shape(h), self._shape(hu), self._shape(hv)
+        _check(lib().swe_set_state(self._h, _p(h), _p(hu), _p(hv)), self._h)
+
+    def step(self, dt, nlevels=1):
+        _check(lib().swe_step(self._h, float(dt), int(nlevels)), self._h)
+
+    def get_state(self, out=None):
+        if out is None:
+            out = tuple(np.zeros((self.K, self.Np)) for _ in range(3))
+        h, hu, hv = out
+        _check(lib().swe_get_state(self._h, _p(h), _p(hu), _p(hv)), self._h)
+        return h, hu, hv
+
+    def get_state_into(self, h, hu, hv):
+        """Write into caller-provided (e.g. pinned) contiguous float64 buffers of K*Np elements."""
+        _check(lib().swe_get_state(self._h, _p(h), _p(hu), _p(hv)), self._h)
+
+    def levels(self):
+        a = np.zeros(self.K, dtype=np.int32)
+        _check(lib().swe_get_levels(self._h, _p(a, C.c_int32)), self._h)
+        return a
+
+    def connectivity(self):
+        e = np.zeros((self.K, 3), dtype=np.int32)
+        f = np.zeros((self.K, 3), dtype=np.int8)
+        _check(lib().swe_get_connectivity(self._h, _p(e, C.c_int32), _p(f, C.c_int8)), self._h)
+        return e, f
+
+    def info(self) -> dict:
+        inf = SweInfo()
+        _check(lib().swe_get_info(self._h, C.byref(inf)), self._h)
+        return {k: (list(getattr(inf, k)) if k == "level_count" else getattr(inf, k)) for k, _ in SweInfo._fields_}
+
+    def profile(self, on: bool):
+        _check(lib().swe_profile(self._h, int(on)), self._h)
+
+    def profile_read(self):
+        t = np.zeros(2)
+        n = np.zeros(2, dtype=np.int64)
+        b = np.zeros(2)
+        _check(lib().swe_profile_read(self._h, _p(t), _p(n, C.c_int64), _p(b)), self._h)
+        return {"k1_ms": t[0], "k2_ms": t[1], "k1_launches": int(n[0]), "k2_launches": int(n[1]),
+                "k1_bytes": b[0], "k2_bytes": b[1]}

@@ -1,0 +1,941 @@
+// solver.cu -- context, MRAB scheduler and C ABI (include/swe.h) of the
+// B200-native DG shallow-water solver.  Device work: kernels.cuh (hot path)
+// plus the setup / permutation / diagnostics kernels below.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/swe.h"
+#include "host.hpp"
+#include "kernels.cuh"
+
+namespace swe {
+
+// ------------------------------------------------------------------ setup kernels
+// a_e of every element from the staged caller-layout state, with IEEE
+// round-to-nearest intrinsics (no FMA contraction), bit-identical to the host
+// expression of element_speeds() (reading A19).
+__global__ void k_speeds(int K, int Np, double g, double e4, double a_floor, const double *h, const double *hu,
+                         const double *hv, double *ae) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= K) return;
+  const double sq2 = 1.4142135623730951;  // == sqrt(2.0) correctly rounded
+  double amax = 0.0;
+  for (int i = 0; i < Np; i++) {
+    size_t k = (size_t)e * Np + i;
+    double hh = h[k];
+    double hp = hh > 0.0 ? hh : 0.0;
+    double h2 = __dmul_rn(hp, hp), h4 = __dmul_rn(h2, h2);
+    double den = __dsqrt_rn(__dadd_rn(h4, h4 > e4 ? h4 : e4));
+    double num = __dmul_rn(sq2, hp);
+    double u = __ddiv_rn(__dmul_rn(num, hu[k]), den), v = __ddiv_rn(__dmul_rn(num, hv[k]), den);
+    double a = __dadd_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v))), __dsqrt_rn(__dmul_rn(g, hp)));
+    amax = a > amax ? a : amax;
+  }
+  ae[e] = a_floor > amax ? a_floor : amax;
+}
+
+// caller layout [K][Np] (3 arrays) -> internal [3][Np][K] in internal order
+__global__ void k_scatter_state(int K, int Np, const int *orig, const double *h, const double *hu, const double *hv,
+                                double *Q) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  size_t e = (size_t)orig[k];
+  for (int i = 0; i < Np; i++) {
+    Q[(size_t)i * K + k] = h[e * Np + i];
+    Q[(size_t)(Np + i) * K + k] = hu[e * Np + i];
+    Q[(size_t)(2 * Np + i) * K + k] = hv[e * Np + i];
+  }
+}
+
+__global__ void k_scatter_field(int K, int Np, const int *orig, const double *src, double *dst) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  size_t e = (size_t)orig[k];
+  for (int i = 0; i < Np; i++) dst[(size_t)i * K + k] = src[e * Np + i];
+}
+
+// internal committed state (parity per level) -> caller layout
+struct GatherParams {
+  int K, Np, nlev, off[9], par[8];
+  const int *orig;
+  const double *Q;
+  double *h, *hu, *hv;
+};
+__global__ void k_gather_state(const __grid_constant__ GatherParams p) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= p.K) return;
+  int c = 0;
+  for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
+  const size_t K = p.K;
+  const double *Q = p.Q + (size_t)p.par[c] * 3 * p.Np * K;
+  size_t e = (size_t)p.orig[k];
+  for (int i = 0; i < p.Np; i++) {
+    p.h[e * p.Np + i] = Q[(size_t)i * K + k];
+    p.hu[e * p.Np + i] = Q[(size_t)(p.Np + i) * K + k];
+    p.hv[e * p.Np + i] = Q[(size_t)(2 * p.Np + i) * K + k];
+  }
+}
+
+// mass and min h per block -> partials[2*block]
+__global__ void k_diag(const __grid_constant__ GatherParams p, const double *V, const double *wm2,
+                       double *partials) {
+  __shared__ double smass[256], smin[256];
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  double mass = 0.0, mn = 1e300;
+  if (k < p.K) {
+    int c = 0;
+    for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
+    const size_t K = p.K;
+    const double *Q = p.Q + (size_t)p.par[c] * 3 * p.Np * K;
+    double x0 = V[k], x1 = V[K + k], x2 = V[2 * K + k], y0 = V[3 * K + k], y1 = V[4 * K + k], y2 = V[5 * K + k];
+    double J = 0.25 * ((x1 - x0) * (y2 - y0) - (x2 - x0) * (y1 - y0));
+    double acc = 0.0;
+    for (int i = 0; i < p.Np; i++) {
+      double h = Q[(size_t)i * K + k];
+      acc += wm2[i] * h;
+      mn = fmin(mn, h);
+    }
+    mass = 2.0 * J * acc;
+  }
+  smass[threadIdx.x] = mass;
+  smin[threadIdx.x] = mn;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      smass[threadIdx.x] += smass[threadIdx.x + s];
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = smass[0];
+    partials[2 * blockIdx.x + 1] = smin[0];
+  }
+}
+
+// ------------------------------------------------------------------ context
+struct Ctx {
+  std::string err;
+  int N = 0, Np = 0, K = 0, device = 0;
+  double g = 9.81;
+  swe_params prm;
+  cudaStream_t stream = 0;
+  RefOps ops;
+  HostMesh mesh;
+  TvbGeom tvb;
+  std::vector<double> Bcaller;  // host copy (caller layout)
+  // device
+  double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
+  double *dTalpha = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
+  double *dBcaller = nullptr, *dPartials = nullptr;
+  int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr;
+  unsigned char *dDry = nullptr;
+  unsigned long long *dCounters = nullptr;
+  unsigned long long *hCounters = nullptr;  // pinned
+  double *hInjected = nullptr;              // pinned
+  // state / schedule
+  bool have_state = false, materialized = false, scheduled = false;
+  double dt = 0.0;
+  int L = 1;
+  std::vector<int32_t> level;      // caller order
+  std::vector<int32_t> order;      // internal k -> caller e
+  int off[9] = {0};
+  int kcount[9] = {0}, par[9] = {0};
+  long tick_s[9] = {0}, t_e[9] = {0};
+  long tick = 0;
+  long n_updates = 0;
+  std::vector<std::pair<int, long>> schedule;  // (level, tick offset) of one macro step
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_kind;
+  double prof_ms[2] = {0, 0}, prof_bytes[2] = {0, 0};
+  long prof_launch[2] = {0, 0};
+  bool alloc_ok = true;
+
+  void *dalloc(size_t bytes) {
+    void *p = nullptr;
+    if (bytes == 0) bytes = 8;
+    if (prm.dev_alloc) {
+      p = prm.dev_alloc(bytes, (void *)stream, prm.alloc_user);
+    } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      p = nullptr;
+    }
+    if (!p) alloc_ok = false;
+    return p;
+  }
+  void dfree(void *p) {
+    if (!p) return;
+    if (prm.dev_free)
+      prm.dev_free(p, (void *)stream, prm.alloc_user);
+    else
+      cudaFree(p);
+  }
+};
+
+static int cuda_fail(Ctx *c, cudaError_t e, const char *where) {
+  c->err = std::string(where) + ": " + cudaGetErrorString(e);
+  return SWE_ERR_CUDA;
+}
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, #call); \
+  } while (0)
+
+template <int N>
+static cudaError_t upload_ops(const RefOps &o) {
+  Ops<N> h;
+  constexpr int Np = Ops<N>::Np, Nc = Ops<N>::Nc, Ng = Ops<N>::Ng, Nfp = Ops<N>::Nfp;
+  for (int c = 0; c < Nc; c++)
+    for (int i = 0; i < Np; i++) {
+      h.Ic[c][i] = o.Ic(c, i);
+      h.IcDr[c][i] = o.IcDr(c, i);
+      h.IcDs[c][i] = o.IcDs(c, i);
+      h.Pr[i][c] = o.Pr(i, c);
+      h.Ps[i][c] = o.Ps(i, c);
+      h.P[i][c] = o.P(i, c);
+    }
+  for (int i = 0; i < Np; i++)
+    for (int g = 0; g < 3 * Ng; g++) h.Lg[i][g] = o.Lg(i, g);
+  for (int j = 0; j < Ng; j++)
+    for (int k = 0; k < Nfp; k++) h.Ig1[j][k] = o.Ig1(j, k);
+  for (int i = 0; i < Np; i++) {
+    h.wm2[i] = 0.5 * o.wmean[i];
+    for (int v = 0; v < 3; v++) h.Pv[v][i] = o.Pv(v, i);
+    h.lam[i][0] = -0.5 * (o.r[i] + o.s[i]);
+    h.lam[i][1] = 0.5 * (1.0 + o.r[i]);
+    h.lam[i][2] = 0.5 * (1.0 + o.s[i]);
+  }
+  const void *sym = N == 1 ? (const void *)&c_ops1
+                           : (N == 2 ? (const void *)&c_ops2 : (N == 3 ? (const void *)&c_ops3 : (const void *)&c_ops4));
+  return cudaMemcpyToSymbol(sym, &h, sizeof(h));
+}
+
+static cudaError_t upload_ops_any(const RefOps &o) {
+  switch (o.N) {
+    case 1: return upload_ops<1>(o);
+    case 2: return upload_ops<2>(o);
+    case 3: return upload_ops<3>(o);
+    case 4: return upload_ops<4>(o);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int N, bool INIT>
+static void launch_k1(const StepParams &p, cudaStream_t s) {
+  int n = p.k1 - p.k0;
+  if (n <= 0) return;
+  k_rhs_update<N, INIT><<<(n + 127) / 128, 128, 0, s>>>(p);
+}
+template <int N>
+static void launch_k2(const StepParams &p, cudaStream_t s) {
+  int n = p.k1 - p.k0;
+  if (n <= 0) return;
+  k_tvb<N><<<(n + 127) / 128, 128, 0, s>>>(p);
+}
+static void launch(int which, bool init, int N, const StepParams &p, cudaStream_t s) {
+  if (which == 0) {
+    switch (N) {
+      case 1: init ? launch_k1<1, true>(p, s) : launch_k1<1, false>(p, s); break;
+      case 2: init ? launch_k1<2, true>(p, s) : launch_k1<2, false>(p, s); break;
+      case 3: init ? launch_k1<3, true>(p, s) : launch_k1<3, false>(p, s); break;
+      case 4: init ? launch_k1<4, true>(p, s) : launch_k1<4, false>(p, s); break;
+    }
+  } else {
+    switch (N) {
+      case 1: launch_k2<1>(p, s); break;
+      case 2: launch_k2<2>(p, s); break;
+      case 3: launch_k2<3>(p, s); break;
+      case 4: launch_k2<4>(p, s); break;
+    }
+  }
+}
+
+// algorithmic bytes per element update
+static double k1_bytes(int N, int nab, bool tvb) {
+  int Np = (N + 1) * (N + 2) / 2, Nfp = N + 1;
+  double d = 3 * Np /*Q r*/ + 3 * Np /*Q w*/ + 3 * Np /*R w*/ + 3 * Np * (nab - 1) /*R r*/ + Np /*B*/ +
+             9 * Nfp /*nbr Q faces*/ + 3 * Nfp /*nbr B faces*/ + 6 /*vertices*/ + 3 /*means w*/ + (tvb ? 9 : 0);
+  return 8.0 * d + 12.0 /*E2E*/ + 1.0 /*dry flag*/;
+}
+static double k2_bytes() { return 8.0 * (3 + 9 + 9 + 6 + 6) + 12.0 + 4.0 + 4.0; }
+
+static StepParams base_params(Ctx *c) {
+  StepParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.K = c->K;
+  p.Q = c->dQ;
+  p.R = c->dR;
+  p.B = c->dB;
+  p.V = c->dV;
+  p.E2E = c->dE2E;
+  p.tcode = c->dTcode;
+  p.talpha = c->dTalpha;
+  p.means = c->dMeans;
+  p.dry = c->dDry;
+  p.UT = c->dUT;
+  p.g = c->g;
+  p.h0 = c->prm.h0;
+  p.eps = c->prm.eps;
+  double e2 = c->prm.eps_u * c->prm.eps_u;
+  p.e4 = e2 * e2;
+  p.tvb_M = c->prm.tvb_M;
+  p.tvb_nu = c->prm.tvb_nu;
+  p.h_char = c->prm.h_char;
+  p.use_pp = c->prm.use_pp;
+  p.use_tvb = c->prm.use_tvb;
+  p.counters = c->dCounters;
+  p.injected = c->dInjected;
+  p.nlev = c->L;
+  for (int l = 0; l <= 8; l++) p.off[l] = c->off[l];
+  return p;
+}
+
+static int alloc_state(Ctx *c) {
+  if (c->dQ) return SWE_OK;
+  size_t K = c->K, Np = c->Np;
+  c->dQ = (double *)c->dalloc(sizeof(double) * 2 * 3 * Np * K);
+  c->dR = (double *)c->dalloc(sizeof(double) * 3 * 3 * Np * K);
+  c->dB = (double *)c->dalloc(sizeof(double) * Np * K);
+  c->dV = (double *)c->dalloc(sizeof(double) * 6 * K);
+  c->dMeans = (double *)c->dalloc(sizeof(double) * 3 * K);
+  c->dUT = (double *)c->dalloc(sizeof(double) * 9 * K);
+  c->dTalpha = (double *)c->dalloc(sizeof(double) * 6 * K);
+  c->dAe = (double *)c->dalloc(sizeof(double) * K);
+  c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * K);
+  c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
+  c->dTcode = (int *)c->dalloc(sizeof(int) * K);
+  c->dOrig = (int *)c->dalloc(sizeof(int) * K);
+  c->dDry = (unsigned char *)c->dalloc(K);
+  c->dPartials = (double *)c->dalloc(sizeof(double) * 2 * ((K + 255) / 256));
+  if (!c->alloc_ok) {
+    c->err = "device allocation failed";
+    return SWE_ERR_NOMEM;
+  }
+  return SWE_OK;
+}
+
+// Build the internal element order for `levels`, upload the static data in
+// that order, scatter the staged (unlimited) state, apply Alg. 2 line 1
+// (M Pi then Lambda Pi on all elements) and reset the MRAB schedule.
+static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
+  const int K = c->K;
+  element_order(c->mesh, levels.data(), c->order);
+  std::vector<int32_t> inv(K);
+  for (int k = 0; k < K; k++) inv[c->order[k]] = k;
+  for (int l = 0; l <= 8; l++) c->off[l] = K;
+  c->off[0] = 0;
+  {
+    std::vector<int> cnt(10, 0);
+    for (int e = 0; e < K; e++) cnt[levels[e]]++;
+    int acc = 0;
+    for (int l = 1; l <= L; l++) {
+      c->off[l - 1] = acc;
+      acc += cnt[l];
+    }
+    for (int l = L; l <= 8; l++) c->off[l] = K;
+  }
+  std::vector<double> V((size_t)6 * K), TA((size_t)6 * K);
+  std::vector<int> E2E((size_t)3 * K), TC(K);
+  for (int k = 0; k < K; k++) {
+    int e = c->order[k];
+    const int32_t *v = &c->mesh.etov[(size_t)3 * e];
+    for (int j = 0; j < 3; j++) {
+      V[(size_t)j * K + k] = c->mesh.vx[v[j]];
+      V[(size_t)(3 + j) * K + k] = c->mesh.vy[v[j]];
+    }
+    int code = 0;
+    for (int f = 0; f < 3; f++) {
+      int n = c->mesh.etoe[(size_t)3 * e + f], nf = c->mesh.etof[(size_t)3 * e + f];
+      E2E[(size_t)f * K + k] = (inv[n] << 2) | nf;
+      size_t s = (size_t)3 * e + f;
+      code |= (c->tvb.pj[s] & 3) << (4 * f);
+      code |= (c->tvb.pk[s] & 3) << (4 * f + 2);
+      TA[(size_t)(2 * f) * K + k] = c->tvb.aj[s];
+      TA[(size_t)(2 * f + 1) * K + k] = c->tvb.ak[s];
+    }
+    TC[k] = code;
+  }
+  CK(cudaMemcpyAsync(c->dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dTalpha, TA.data(), sizeof(double) * TA.size(), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dE2E, E2E.data(), sizeof(int) * E2E.size(), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dTcode, TC.data(), sizeof(int) * TC.size(), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dOrig, c->order.data(), sizeof(int) * K, cudaMemcpyHostToDevice, c->stream));
+  int nb = (K + 127) / 128;
+  k_scatter_field<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dBcaller, c->dB);
+  const size_t KNp = (size_t)K * c->Np;
+  k_scatter_state<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp, c->dStage + 2 * KNp,
+                                             c->dQ);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
+  // schedule reset
+  c->L = L;
+  for (int l = 0; l <= 8; l++) {
+    c->kcount[l] = 0;
+    c->par[l] = 0;
+    c->tick_s[l] = 0;
+    c->t_e[l] = 0;
+  }
+  c->tick = 0;
+  // Alg. 2 line 1: M Pi then Lambda Pi on every element, in place in Q[0]
+  StepParams p = base_params(c);
+  p.k0 = 0;
+  p.k1 = K;
+  p.nlev = 1;
+  for (int l = 1; l <= 8; l++) p.off[l] = K;
+  p.own_par = 0;
+  p.write_par = 0;
+  launch(0, true, c->N, p, c->stream);
+  if (c->prm.use_tvb) launch(1, false, c->N, p, c->stream);
+  CK(cudaGetLastError());
+  c->materialized = true;
+  return SWE_OK;
+}
+
+// recursive slowest-first macro step (reading A17):
+// S(l, t) = [(l, t)] + S(l-1, t) + S(l-1, t + 2^(l-2))
+static void build_schedule(int l, long t, std::vector<std::pair<int, long>> &out) {
+  out.push_back({l, t});
+  if (l > 1) {
+    build_schedule(l - 1, t, out);
+    build_schedule(l - 1, t + (1L << (l - 2)), out);
+  }
+}
+
+static void ab_weights(int m, double a[3]) {
+  a[0] = a[1] = a[2] = 0.0;
+  if (m <= 1) {
+    a[0] = 1.0;
+  } else if (m == 2) {
+    a[0] = 1.5;
+    a[1] = -0.5;
+  } else {
+    a[0] = 23.0 / 12.0;
+    a[1] = -16.0 / 12.0;
+    a[2] = 5.0 / 12.0;
+  }
+}
+// integral over [0, theta] of the quadratic interpolant of R(0), R(-1), R(-2)
+static void dense_weights(int m, double th, double b[3]) {
+  b[0] = b[1] = b[2] = 0.0;
+  double t2 = th * th, t3 = t2 * th;
+  if (m <= 1) {
+    b[0] = th;
+  } else if (m == 2) {
+    b[0] = th + 0.5 * t2;
+    b[1] = -0.5 * t2;
+  } else {
+    b[0] = t3 / 6.0 + 0.75 * t2 + th;
+    b[1] = -t3 / 3.0 - t2;
+    b[2] = t3 / 6.0 + 0.25 * t2;
+  }
+}
+
+static int run_update(Ctx *c, int l, long t) {
+  StepParams p = base_params(c);
+  p.k0 = c->off[l - 1];
+  p.k1 = c->off[l];
+  const double dtl = std::ldexp(c->dt, l - 1);
+  const int k = c->kcount[l];
+  const int m = std::min(k + 1, 3);
+  double a[3];
+  ab_weights(m, a);
+  p.own_par = c->par[l];
+  p.write_par = 1 - c->par[l];
+  p.write_slot = k % 3;
+  p.nab = m;
+  for (int s = 0; s < 3; s++) {
+    p.ab[s] = a[s] * dtl;
+    p.ab_slot[s] = ((k - s) % 3 + 3) % 3;
+  }
+  for (int cl = 1; cl <= c->L; cl++) {
+    LevelTab &T = p.lev[cl - 1];
+    if (c->t_e[cl] == t) {
+      T.par = c->par[cl];
+      T.dense = 0;
+    } else {  // coarser level in the middle of its step
+      T.par = 1 - c->par[cl];
+      long step = c->t_e[cl] - c->tick_s[cl];
+      double theta = (double)(t - c->tick_s[cl]) / (double)step;
+      if (t == c->tick_s[cl]) {
+        T.dense = 0;
+      } else {
+        T.dense = 1;
+        T.nterm = std::min(c->kcount[cl], 3);
+        double b[3];
+        dense_weights(T.nterm, theta, b);
+        double dtc = std::ldexp(c->dt, cl - 1);
+        for (int s = 0; s < 3; s++) {
+          T.beta[s] = b[s] * dtc;
+          T.slot[s] = ((c->kcount[cl] - 1 - s) % 3 + 3) % 3;
+        }
+      }
+    }
+  }
+  const int nel = p.k1 - p.k0;
+  if (c->prof && nel > 0) {
+    size_t i0 = c->ev.size();
+    for (int j = 0; j < 4; j++) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->ev.push_back(e);
+    }
+    cudaEventRecord(c->ev[i0], c->stream);
+    launch(0, false, c->N, p, c->stream);
+    cudaEventRecord(c->ev[i0 + 1], c->stream);
+    c->prof_bytes[0] += k1_bytes(c->N, m, c->prm.use_tvb) * nel;
+    c->prof_launch[0]++;
+    if (c->prm.use_tvb) {
+      cudaEventRecord(c->ev[i0 + 2], c->stream);
+      launch(1, false, c->N, p, c->stream);
+      cudaEventRecord(c->ev[i0 + 3], c->stream);
+      c->prof_bytes[1] += k2_bytes() * nel;
+      c->prof_launch[1]++;
+    } else {
+      cudaEventRecord(c->ev[i0 + 2], c->stream);
+      cudaEventRecord(c->ev[i0 + 3], c->stream);
+    }
+  } else {
+    launch(0, false, c->N, p, c->stream);
+    if (c->prm.use_tvb) launch(1, false, c->N, p, c->stream);
+  }
+  c->n_updates += nel;
+  c->par[l] ^= 1;
+  c->kcount[l] = k + 1;
+  c->tick_s[l] = t;
+  c->t_e[l] = t + (1L << (l - 1));
+  return SWE_OK;
+}
+
+static void collect_profile(Ctx *c) {
+  for (size_t i = 0; i + 3 < c->ev.size(); i += 4) {
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, c->ev[i], c->ev[i + 1]);
+    cudaEventElapsedTime(&b, c->ev[i + 2], c->ev[i + 3]);
+    c->prof_ms[0] += a;
+    c->prof_ms[1] += b;
+  }
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  c->ev.clear();
+}
+
+static GatherParams gather_params(Ctx *c, double *h, double *hu, double *hv) {
+  GatherParams g;
+  std::memset(&g, 0, sizeof(g));
+  g.K = c->K;
+  g.Np = c->Np;
+  g.nlev = c->L;
+  for (int l = 0; l <= 8; l++) g.off[l] = c->off[l];
+  for (int l = 1; l <= 8; l++) g.par[l - 1] = c->par[l];
+  g.orig = c->dOrig;
+  g.Q = c->dQ;
+  g.h = h;
+  g.hu = hu;
+  g.hv = hv;
+  return g;
+}
+
+}  // namespace swe
+
+using namespace swe;
+
+struct swe_ctx {
+  Ctx c;
+};
+
+extern "C" {
+
+static void fill_defaults(swe_params &p, const swe_params *in) {
+  std::memset(&p, 0, sizeof(p));
+  if (in) {
+    p = *in;
+  } else {
+    p.use_pp = 1;
+    p.use_tvb = 1;
+  }
+  if (!(p.h0 > 0)) p.h0 = 1e-6;
+  if (!(p.eps > 0)) p.eps = p.h0;
+  if (!(p.tvb_nu > 0)) p.tvb_nu = 1.5;
+  if (!(p.eps_u > 0)) p.eps_u = 1000.0 * p.h0;
+  if (!(p.h_char > 0)) p.h_char = 10.0 * p.h0;
+  if (p.a_floor < 0) p.a_floor = 0;
+  if (p.tvb_M < 0) p.tvb_M = 0;
+}
+
+int swe_nodes(const swe_mesh *mesh, int N, double *x, double *y) {
+  if (!mesh || !x || !y || !mesh->etov || !mesh->vx || !mesh->vy || mesh->nelems <= 0) return SWE_ERR_ARG;
+  if (N < 1 || N > 8) return SWE_ERR_ORDER;
+  HostMesh m;
+  std::string err;
+  int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, m, &err);
+  if (rc) return rc;
+  RefOps o;
+  if (!build_refops(N, o, &err)) return SWE_ERR_ORDER;
+  for (int e = 0; e < m.K; e++) {
+    const int32_t *v = &m.etov[(size_t)3 * e];
+    double x1 = m.vx[v[0]], x2 = m.vx[v[1]], x3 = m.vx[v[2]], y1 = m.vy[v[0]], y2 = m.vy[v[1]], y3 = m.vy[v[2]];
+    for (int i = 0; i < o.Np; i++) {
+      double r = o.r[i], s = o.s[i];
+      x[(size_t)e * o.Np + i] = -0.5 * (r + s) * x1 + 0.5 * (1.0 + r) * x2 + 0.5 * (1.0 + s) * x3;
+      y[(size_t)e * o.Np + i] = -0.5 * (r + s) * y1 + 0.5 * (1.0 + r) * y2 + 0.5 * (1.0 + s) * y3;
+    }
+  }
+  return SWE_OK;
+}
+
+int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe_params *params, swe_ctx **out) {
+  if (!out) return SWE_ERR_ARG;
+  *out = nullptr;
+  if (!mesh || !B || !mesh->etov || !mesh->vx || !mesh->vy || mesh->nelems <= 0 || mesh->nverts <= 0 || !(g > 0))
+    return SWE_ERR_ARG;
+  if (N < 1 || N > kMaxOrder) return SWE_ERR_ORDER;
+  swe_ctx *h = new swe_ctx();
+  Ctx *c = &h->c;
+  fill_defaults(c->prm, params);
+  c->N = N;
+  c->Np = (N + 1) * (N + 2) / 2;
+  c->K = mesh->nelems;
+  c->g = g;
+  c->device = c->prm.device;
+  c->stream = (cudaStream_t)c->prm.stream;
+  auto fail = [&](int rc) {
+    swe_destroy(h);
+    return rc;
+  };
+  int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, c->mesh, &c->err);
+  if (rc) return fail(rc);
+  if (!build_refops(N, c->ops, &c->err)) return fail(SWE_ERR_ORDER);
+  for (int f = 0; f < 3; f++)
+    for (int k = 0; k < c->ops.Nfp; k++)
+      if (c->ops.Fmask[f * c->ops.Nfp + k] != fmask(N, f, k)) {
+        c->err = "face node table mismatch";
+        return fail(SWE_ERR_ORDER);
+      }
+  build_tvb_geometry(c->mesh, c->tvb);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    c->err = "no CUDA device";
+    cudaGetLastError();
+    return fail(SWE_ERR_CUDA);
+  }
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(SWE_ERR_CUDA);
+  if (upload_ops_any(c->ops) != cudaSuccess) return fail(SWE_ERR_CUDA);
+  rc = alloc_state(c);
+  if (rc) return fail(rc);
+  c->dBcaller = (double *)c->dalloc(sizeof(double) * (size_t)c->K * c->Np);
+  c->dWm2 = (double *)c->dalloc(sizeof(double) * c->Np);
+  c->dCounters = (unsigned long long *)c->dalloc(sizeof(unsigned long long) * 8);
+  c->dInjected = (double *)c->dalloc(sizeof(double));
+  if (!c->alloc_ok) return fail(SWE_ERR_NOMEM);
+  if (cudaMallocHost(&c->hCounters, sizeof(unsigned long long) * 8) != cudaSuccess) return fail(SWE_ERR_CUDA);
+  if (cudaMallocHost(&c->hInjected, sizeof(double)) != cudaSuccess) return fail(SWE_ERR_CUDA);
+  std::vector<double> wm2(c->Np);
+  for (int i = 0; i < c->Np; i++) wm2[i] = 0.5 * c->ops.wmean[i];
+  if (cudaMemcpyAsync(c->dBcaller, B, sizeof(double) * (size_t)c->K * c->Np, cudaMemcpyHostToDevice, c->stream) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(c->dWm2, wm2.data(), sizeof(double) * c->Np, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    c->err = "initial upload failed";
+    return fail(SWE_ERR_CUDA);
+  }
+  *out = h;
+  return SWE_OK;
+}
+
+int swe_set_state(swe_ctx *h, const double *hh, const double *hu, const double *hv) {
+  if (!h || !hh || !hu || !hv) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  const size_t KNp = (size_t)c->K * c->Np;
+  CK(cudaMemcpyAsync(c->dStage, hh, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dStage + KNp, hu, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dStage + 2 * KNp, hv, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
+  double e2 = c->prm.eps_u * c->prm.eps_u, e4 = e2 * e2;
+  k_speeds<<<(c->K + 127) / 128, 128, 0, c->stream>>>(c->K, c->Np, c->g, e4, c->prm.a_floor, c->dStage,
+                                                       c->dStage + KNp, c->dStage + 2 * KNp, c->dAe);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream));
+  CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream));
+  c->have_state = true;
+  c->materialized = false;
+  c->scheduled = false;
+  c->n_updates = 0;
+  c->tick = 0;
+  return SWE_OK;
+}
+
+int swe_step(swe_ctx *h, double dt, int nlevels) {
+  if (!h) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  if (!c->have_state) {
+    c->err = "swe_step before swe_set_state";
+    return SWE_ERR_STATE;
+  }
+  if (!(dt > 0) || !std::isfinite(dt) || nlevels < 1 || nlevels > 8) {
+    c->err = "invalid dt or nlevels";
+    return SWE_ERR_ARG;
+  }
+  if (!c->scheduled) {
+    std::vector<double> ae(c->K);
+    CK(cudaMemcpyAsync(ae.data(), c->dAe, sizeof(double) * c->K, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->level.assign(c->K, 1);
+    bin_levels(c->K, c->mesh.hk.data(), ae.data(), nlevels, c->level.data());
+    int rc = materialize(c, c->level, nlevels);
+    if (rc) return rc;
+    c->scheduled = true;
+    c->dt = dt;
+    c->L = nlevels;
+    c->schedule.clear();
+    build_schedule(nlevels, 0, c->schedule);
+  } else if (dt != c->dt || nlevels != c->L) {
+    c->err = "(dt, nlevels) differ from the first swe_step (levels are fixed, P:149)";
+    return SWE_ERR_SCHEDULE;
+  }
+  for (auto &st : c->schedule) {
+    int rc = run_update(c, st.first, c->tick + st.second);
+    if (rc) return rc;
+  }
+  c->tick += 1L << (c->L - 1);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->prof) collect_profile(c);
+  if (c->hCounters[3] != 0) {
+    c->err = "non-finite values produced";
+    return SWE_ERR_NONFINITE;
+  }
+  return SWE_OK;
+}
+
+static int ensure_materialized(Ctx *c) {
+  if (c->materialized) return SWE_OK;
+  std::vector<int32_t> ones(c->K, 1);
+  return materialize(c, ones, 1);
+}
+
+int swe_get_state(swe_ctx *h, double *hh, double *hu, double *hv) {
+  if (!h || !hh || !hu || !hv) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  if (!c->have_state) return SWE_ERR_STATE;
+  int rc = ensure_materialized(c);
+  if (rc) return rc;
+  const size_t KNp = (size_t)c->K * c->Np;
+  // gather into the staging buffer's twin: reuse dR slot 2's space is unsafe; use a temporary
+  double *tmp = (double *)c->dalloc(sizeof(double) * 3 * KNp);
+  if (!tmp) return SWE_ERR_NOMEM;
+  GatherParams g = gather_params(c, tmp, tmp + KNp, tmp + 2 * KNp);
+  k_gather_state<<<(c->K + 127) / 128, 128, 0, c->stream>>>(g);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hh, tmp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hu, tmp + KNp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(hv, tmp + 2 * KNp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  c->dfree(tmp);
+  if (e != cudaSuccess) return cuda_fail(c, e, "swe_get_state");
+  return SWE_OK;
+}
+
+void swe_destroy(swe_ctx *h) {
+  if (!h) return;
+  Ctx *c = &h->c;
+  if (c->stream || c->dQ) cudaStreamSynchronize(c->stream);
+  void *ptrs[] = {c->dQ, c->dR, c->dB, c->dV, c->dMeans, c->dUT, c->dTalpha, c->dAe, c->dStage, c->dInjected,
+                  c->dWm2, c->dBcaller, c->dPartials, c->dE2E, c->dTcode, c->dOrig, c->dDry, c->dCounters};
+  for (void *p : ptrs) c->dfree(p);
+  if (c->hCounters) cudaFreeHost(c->hCounters);
+  if (c->hInjected) cudaFreeHost(c->hInjected);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  delete h;
+}
+
+int swe_get_levels(swe_ctx *h, int32_t *level) {
+  if (!h || !level) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  if (!c->scheduled) return SWE_ERR_STATE;
+  std::copy(c->level.begin(), c->level.end(), level);
+  return SWE_OK;
+}
+
+int swe_get_connectivity(const swe_ctx *h, int32_t *etoe, int8_t *etof) {
+  if (!h || !etoe || !etof) return SWE_ERR_ARG;
+  const Ctx *c = &h->c;
+  std::copy(c->mesh.etoe.begin(), c->mesh.etoe.end(), etoe);
+  std::copy(c->mesh.etof.begin(), c->mesh.etof.end(), etof);
+  return SWE_OK;
+}
+
+int swe_get_info(swe_ctx *h, swe_info *info) {
+  if (!h || !info) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  std::memset(info, 0, sizeof(*info));
+  info->K = c->K;
+  info->Np = c->Np;
+  info->N = c->N;
+  info->nflipped = c->mesh.nflipped;
+  info->nlevels = c->scheduled ? c->L : 0;
+  info->t = c->scheduled ? c->dt * (double)c->tick : 0.0;
+  info->n_updates = c->n_updates;
+  if (c->scheduled)
+    for (int l = 1; l <= c->L; l++) info->level_count[l - 1] = c->off[l] - c->off[l - 1];
+  if (!c->have_state) return SWE_OK;
+  int rc = ensure_materialized(c);
+  if (rc) return rc;
+  int nb = (c->K + 255) / 256;
+  GatherParams g = gather_params(c, nullptr, nullptr, nullptr);
+  k_diag<<<nb, 256, 0, c->stream>>>(g, c->dV, c->dWm2, c->dPartials);
+  std::vector<double> part(2 * (size_t)nb);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(part.data(), c->dPartials, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hInjected, c->dInjected, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  double mass = 0.0, mn = 1e300;
+  for (int b = 0; b < nb; b++) {
+    mass += part[2 * b];
+    mn = std::min(mn, part[2 * b + 1]);
+  }
+  info->mass = mass;
+  info->min_h = mn;
+  info->injected_mass = *c->hInjected;
+  info->n_pp = (int64_t)c->hCounters[0];
+  info->n_dry = (int64_t)c->hCounters[1];
+  info->n_tvb = (int64_t)c->hCounters[2];
+  return SWE_OK;
+}
+
+const char *swe_last_error(const swe_ctx *h) { return h ? h->c.err.c_str() : "null context"; }
+
+int swe_profile(swe_ctx *h, int on) {
+  if (!h) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  c->prof = on != 0;
+  if (on) {
+    c->prof_ms[0] = c->prof_ms[1] = 0;
+    c->prof_bytes[0] = c->prof_bytes[1] = 0;
+    c->prof_launch[0] = c->prof_launch[1] = 0;
+  }
+  return SWE_OK;
+}
+
+int swe_profile_read(swe_ctx *h, double *times_ms, int64_t *launches, double *bytes) {
+  if (!h) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  for (int i = 0; i < 2; i++) {
+    if (times_ms) times_ms[i] = c->prof_ms[i];
+    if (launches) launches[i] = c->prof_launch[i];
+    if (bytes) bytes[i] = c->prof_bytes[i];
+  }
+  return SWE_OK;
+}
+
+// ------------------------------------------------------------------ host-only builders
+int swe_host_refel(int N, const char *name, double *out, int32_t *rows, int32_t *cols) {
+  if (!name) return SWE_ERR_ARG;
+  RefOps o;
+  std::string err;
+  if (!build_refops(N, o, &err)) return SWE_ERR_ORDER;
+  std::string n(name);
+  std::vector<double> v;
+  int r = 0, cc = 1;
+  auto vec = [&](const std::vector<double> &a) {
+    v = a;
+    r = (int)a.size();
+    cc = 1;
+  };
+  auto mat = [&](const DMat &m) {
+    v = m.a;
+    r = m.rows;
+    cc = m.cols;
+  };
+  if (n == "r") vec(o.r);
+  else if (n == "s") vec(o.s);
+  else if (n == "rc") vec(o.rc);
+  else if (n == "sc") vec(o.sc);
+  else if (n == "wc") vec(o.wc);
+  else if (n == "tg") vec(o.tg);
+  else if (n == "wg") vec(o.wg);
+  else if (n == "wmean") vec(o.wmean);
+  else if (n == "Dr") mat(o.Dr);
+  else if (n == "Ds") mat(o.Ds);
+  else if (n == "Mref") mat(o.Mref);
+  else if (n == "Ic") mat(o.Ic);
+  else if (n == "Ig") mat(o.Ig);
+  else if (n == "P") mat(o.P);
+  else if (n == "Pr") mat(o.Pr);
+  else if (n == "Ps") mat(o.Ps);
+  else if (n == "Lg") mat(o.Lg);
+  else if (n == "Pv") mat(o.Pv);
+  else if (n == "Ig1") mat(o.Ig1);
+  else return SWE_ERR_ARG;
+  if (rows) *rows = r;
+  if (cols) *cols = cc;
+  if (out) std::copy(v.begin(), v.end(), out);
+  return SWE_OK;
+}
+
+int swe_host_connectivity(const swe_mesh *mesh, int32_t *etoe, int8_t *etof, int32_t *nflipped) {
+  if (!mesh || !etoe || !etof) return SWE_ERR_ARG;
+  HostMesh m;
+  std::string err;
+  int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, m, &err);
+  if (rc) return rc;
+  std::copy(m.etoe.begin(), m.etoe.end(), etoe);
+  std::copy(m.etof.begin(), m.etof.end(), etof);
+  if (nflipped) *nflipped = m.nflipped;
+  return SWE_OK;
+}
+
+int swe_host_hk(const swe_mesh *mesh, double *hk) {
+  if (!mesh || !hk) return SWE_ERR_ARG;
+  HostMesh m;
+  std::string err;
+  int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, m, &err);
+  if (rc) return rc;
+  std::copy(m.hk.begin(), m.hk.end(), hk);
+  return SWE_OK;
+}
+
+int swe_host_levels(const swe_mesh *mesh, int N, double g, const double *h, const double *hu, const double *hv,
+                    const swe_params *params, int nlevels, int32_t *level) {
+  if (!mesh || !h || !hu || !hv || !level || nlevels < 1 || nlevels > 8) return SWE_ERR_ARG;
+  if (N < 1 || N > 8) return SWE_ERR_ORDER;
+  HostMesh m;
+  std::string err;
+  int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, m, &err);
+  if (rc) return rc;
+  swe_params p;
+  fill_defaults(p, params);
+  int Np = (N + 1) * (N + 2) / 2;
+  std::vector<double> ae(m.K);
+  element_speeds(m.K, Np, g, p.eps_u, p.a_floor, h, hu, hv, ae.data());
+  bin_levels(m.K, m.hk.data(), ae.data(), nlevels, level);
+  return SWE_OK;
+}
+
+int swe_host_tvb_geometry(const swe_mesh *mesh, int32_t *pairs, double *alphas) {
+  if (!mesh || !pairs || !alphas) return SWE_ERR_ARG;
+  HostMesh m;
+  std::string err;
+  int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, m, &err);
+  if (rc) return rc;
+  TvbGeom t;
+  build_tvb_geometry(m, t);
+  for (size_t i = 0; i < (size_t)3 * m.K; i++) {
+    pairs[2 * i] = t.pj[i];
+    pairs[2 * i + 1] = t.pk[i];
+    alphas[2 * i] = t.aj[i];
+    alphas[2 * i + 1] = t.ak[i];
+  }
+  return SWE_OK;
+}
+
+}  // extern "C"
