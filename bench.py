@@ -171,8 +171,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--base-n", type=int, default=1280)
-    ap.add_argument("--cpu-strip", type=int, default=32)
-    ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--cpu-strip", type=int, default=4)
+    ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()

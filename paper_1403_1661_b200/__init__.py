@@ -202,7 +202,10 @@ class _TorchAllocator:
             return int(torch.cuda.caching_allocator_alloc(int(nbytes), self.device, stream))
 
         def _free(ptr, stream, user):
-            torch.cuda.caching_allocator_delete(ptr)
+            try:
+                torch.cuda.caching_allocator_delete(ptr)
+            except Exception:  # interpreter shutdown: the allocator is gone with the process
+                pass
 
         self.alloc = ALLOC_FN(_alloc)
         self.free = FREE_FN(_free)

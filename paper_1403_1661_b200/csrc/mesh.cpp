@@ -239,13 +239,14 @@ void bin_levels(int K, const double *hk, const double *ae, int L, int32_t *level
   }
 }
 
+// 2D Morton: spread the low 21 bits of v to the even bit positions (42-bit key).
 static uint64_t spread_bits(uint32_t v) {
   uint64_t x = v & 0x1fffff;
-  x = (x | (x << 32)) & 0x1f00000000ffffULL;
-  x = (x | (x << 16)) & 0x1f0000ff0000ffULL;
-  x = (x | (x << 8)) & 0x100f00f00f00f00fULL;
-  x = (x | (x << 4)) & 0x10c30c30c30c30c3ULL;
-  x = (x | (x << 2)) & 0x1249249249249249ULL;
+  x = (x | (x << 16)) & 0x0000ffff0000ffffULL;
+  x = (x | (x << 8)) & 0x00ff00ff00ff00ffULL;
+  x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0fULL;
+  x = (x | (x << 2)) & 0x3333333333333333ULL;
+  x = (x | (x << 1)) & 0x5555555555555555ULL;
   return x;
 }
 
@@ -267,7 +268,7 @@ void element_order(const HostMesh &m, const int32_t *level, std::vector<int32_t>
     uint32_t ix = (uint32_t)((bx - xmin) * sx), iy = (uint32_t)((by - ymin) * sy);
     uint64_t morton = spread_bits(ix) | (spread_bits(iy) << 1);
     uint64_t lev = level ? (uint64_t)(level[e] - 1) : 0;
-    keys[e] = {(lev << 60) | morton, e};
+    keys[e] = {(lev << 48) | morton, e};  // level field above the 42 Morton bits
   }
   std::sort(keys.begin(), keys.end());
   order.resize(K);

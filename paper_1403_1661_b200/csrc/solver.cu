@@ -132,7 +132,7 @@ struct Ctx {
   // device
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
   double *dTalpha = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
-  double *dBcaller = nullptr, *dPartials = nullptr;
+  double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr;
   int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr;
   unsigned char *dDry = nullptr;
   unsigned long long *dCounters = nullptr;
@@ -217,6 +217,35 @@ static cudaError_t upload_ops(const RefOps &o) {
   return cudaMemcpyToSymbol(sym, &h, sizeof(h));
 }
 
+template <int N>
+static std::vector<double> smem_ops(const RefOps &o) {
+  using SO = SmemOps<N>;
+  std::vector<double> v(SO::total, 0.0);
+  for (int c = 0; c < SO::Nc; c++)
+    for (int i = 0; i < SO::Np; i++) {
+      v[SO::Ic + c * SO::NpP + i] = o.Ic(c, i);
+      v[SO::IcDr + c * SO::NpP + i] = o.IcDr(c, i);
+      v[SO::IcDs + c * SO::NpP + i] = o.IcDs(c, i);
+      v[SO::PrT + c * SO::NpP + i] = o.Pr(i, c);
+      v[SO::PsT + c * SO::NpP + i] = o.Ps(i, c);
+      v[SO::PT + c * SO::NpP + i] = o.P(i, c);
+    }
+  for (int g = 0; g < 3 * SO::Ng; g++)
+    for (int i = 0; i < SO::Np; i++) v[SO::LgT + g * SO::NpP + i] = o.Lg(i, g);
+  for (int j = 0; j < SO::Ng; j++)
+    for (int k = 0; k < SO::Nfp; k++) v[SO::Ig1 + j * SO::NfpP + k] = o.Ig1(j, k);
+  return v;
+}
+static std::vector<double> smem_ops_any(const RefOps &o) {
+  switch (o.N) {
+    case 1: return smem_ops<1>(o);
+    case 2: return smem_ops<2>(o);
+    case 3: return smem_ops<3>(o);
+    case 4: return smem_ops<4>(o);
+  }
+  return {};
+}
+
 static cudaError_t upload_ops_any(const RefOps &o) {
   switch (o.N) {
     case 1: return upload_ops<1>(o);
@@ -231,7 +260,8 @@ template <int N, bool INIT>
 static void launch_k1(const StepParams &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
-  k_rhs_update<N, INIT><<<(n + 127) / 128, 128, 0, s>>>(p);
+  size_t smem = INIT ? 0 : sizeof(double) * SmemOps<N>::total;
+  k_rhs_update<N, INIT><<<(n + 127) / 128, 128, smem, s>>>(p);
 }
 template <int N>
 static void launch_k2(const StepParams &p, cudaStream_t s) {
@@ -292,6 +322,7 @@ static StepParams base_params(Ctx *c) {
   p.use_tvb = c->prm.use_tvb;
   p.counters = c->dCounters;
   p.injected = c->dInjected;
+  p.opsG = c->dOpsG;
   p.nlev = c->L;
   for (int l = 0; l <= 8; l++) p.off[l] = c->off[l];
   return p;
@@ -327,6 +358,11 @@ static int alloc_state(Ctx *c) {
 static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   const int K = c->K;
   element_order(c->mesh, levels.data(), c->order);
+  for (int k = 1; k < K; k++)
+    if (levels[c->order[k]] < levels[c->order[k - 1]]) {
+      c->err = "internal element order is not level-major";
+      return SWE_ERR_SCHEDULE;
+    }
   std::vector<int32_t> inv(K);
   for (int k = 0; k < K; k++) inv[c->order[k]] = k;
   for (int l = 0; l <= 8; l++) c->off[l] = K;
@@ -374,6 +410,10 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
                                              c->dQ);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
+  // counters count from the (re-)application of Alg. 2 line 1
+  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream));
+  CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream));
+  c->n_updates = 0;
   // schedule reset
   c->L = L;
   for (int l = 0; l <= 8; l++) {
@@ -630,6 +670,8 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   if (rc) return fail(rc);
   c->dBcaller = (double *)c->dalloc(sizeof(double) * (size_t)c->K * c->Np);
   c->dWm2 = (double *)c->dalloc(sizeof(double) * c->Np);
+  std::vector<double> sops = smem_ops_any(c->ops);
+  c->dOpsG = (double *)c->dalloc(sizeof(double) * sops.size());
   c->dCounters = (unsigned long long *)c->dalloc(sizeof(unsigned long long) * 8);
   c->dInjected = (double *)c->dalloc(sizeof(double));
   if (!c->alloc_ok) return fail(SWE_ERR_NOMEM);
@@ -640,6 +682,8 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   if (cudaMemcpyAsync(c->dBcaller, B, sizeof(double) * (size_t)c->K * c->Np, cudaMemcpyHostToDevice, c->stream) !=
           cudaSuccess ||
       cudaMemcpyAsync(c->dWm2, wm2.data(), sizeof(double) * c->Np, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->dOpsG, sops.data(), sizeof(double) * sops.size(), cudaMemcpyHostToDevice, c->stream) !=
+          cudaSuccess ||
       cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream) != cudaSuccess ||
       cudaStreamSynchronize(c->stream) != cudaSuccess) {
@@ -749,7 +793,7 @@ void swe_destroy(swe_ctx *h) {
   Ctx *c = &h->c;
   if (c->stream || c->dQ) cudaStreamSynchronize(c->stream);
   void *ptrs[] = {c->dQ, c->dR, c->dB, c->dV, c->dMeans, c->dUT, c->dTalpha, c->dAe, c->dStage, c->dInjected,
-                  c->dWm2, c->dBcaller, c->dPartials, c->dE2E, c->dTcode, c->dOrig, c->dDry, c->dCounters};
+                  c->dWm2, c->dBcaller, c->dPartials, c->dOpsG, c->dE2E, c->dTcode, c->dOrig, c->dDry, c->dCounters};
   for (void *p : ptrs) c->dfree(p);
   if (c->hCounters) cudaFreeHost(c->hCounters);
   if (c->hInjected) cudaFreeHost(c->hInjected);
