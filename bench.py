@@ -197,21 +197,36 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     P.lib()
 
-    # ---- workload (C5, weak scaling: each rank owns a 2000 km x 2000 km basin strip of the P-wide domain)
+    # ---- workload: C5 tsunami basin.  N=1: the full 2000 km x 2000 km basin.  N>1 (weak scaling):
+    # a 2000 km x (2000 km * N) basin, rank r owns the r-th 2000 km y-strip; every rank generates its
+    # strip plus two buffer rows, ghosts are refreshed by NCCL halo exchanges after every level update.
     t_setup = time.time()
-    w = workload(1, args.base_n)
+    if world > 1:
+        w, owner, gid = si.c5_rank_strip(rank, world, args.base_n)
+        idbuf = [P.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(idbuf, src=0)
+        part = dict(rank=rank, nranks=world, owner=owner, gid=gid, nccl_id=idbuf[0])
+    else:
+        w = workload(1, args.base_n)
+        owner = None
+        part = {}
     m = w.mesh
     N, Np, L = 3, 10, w.nlevels
     x, y = P.nodes(m.vx, m.vy, m.etov, N)
     B, h, hu, hv = w.fields(x, y)
     del x, y
-    s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=w.params, device=local)
+    s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=w.params, device=local, **part)
     dt = si.dt_for(m, N, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
+    if world > 1:
+        tdt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tdt, op=torch.distributed.ReduceOp.MIN)
+        dt = float(tdt.item())
     s.set_state(h, hu, hv)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         s.step(dt, L)
-    lev = s.levels()
+    lev_all = s.levels()
+    lev = lev_all if owner is None else lev_all[owner == rank]
     U = dof_per_macro_step(lev, L, Np)
     t_setup = time.time() - t_setup
 
@@ -236,7 +251,12 @@ def main():
         ms = float(t.item())
         torch.distributed.barrier()
     ms_per_step = ms / args.steps
-    value = U * world * args.steps / (ms / 1e3)
+    U_all = U
+    if world > 1:
+        tu = torch.tensor([float(U)], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tu)
+        U_all = int(tu.item())
+    value = U_all * args.steps / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (K1), algorithmic bytes / event-timed launch duration
     peak, peak_kind = load_peaks()
@@ -270,7 +290,7 @@ def main():
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         state_bytes = 3 * h.size * 8
-        e2e = {"value": U * world * args.e2e_steps / el, "unit": UNIT,
+        e2e = {"value": U_all * args.e2e_steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(state_bytes / args.e2e_steps), "d2h_bytes_per_step": int(state_bytes),
                "note": "set_state (H2D, incl. level binning + initial limiting) once, then per macro step swe_step + "
                        "swe_get_state (D2H) into pinned host buffers; wall clock"}
@@ -284,10 +304,11 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C5 synthetic tsunami basin (SURVEY 8(d)), N=3, 4 MRAB levels, PP+TVB",
-                       "K": int(m.K), "level_counts": [int(c) for c in np.bincount(lev, minlength=L + 1)[1:]],
-                       "dof_updates_per_step": U, "dt": dt, "l2": "inputs larger than L2 (state+history ~13 GB)",
-                       "setup_s": round(t_setup, 1)},
+            "config": {"workload": "C5 synthetic tsunami basin (SURVEY 8(d)), N=3, 4 MRAB levels, PP+TVB"
+                                   + (f", {world} y-strips (weak scaling, NCCL halo exchange)" if world > 1 else ""),
+                       "K_per_rank": int(len(lev)), "level_counts": [int(c) for c in np.bincount(lev, minlength=L + 1)[1:]],
+                       "dof_updates_per_step": U_all, "dt": dt, "l2": "inputs larger than L2 (state+history ~13 GB/rank)",
+                       "parallelism": f"element partition x{world}", "setup_s": round(t_setup, 1)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(prof["k1_launches"] + prof["k2_launches"]),
             "clocks": clk.summary(),

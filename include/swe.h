@@ -73,7 +73,7 @@ typedef struct {
   double a_floor;  /* lower bound of the wave speed used for level binning, default 0 */
   double eps_u;    /* velocity desingularisation scale, default 1000*h0 (A4') */
   double h_char;   /* below this mean depth TVB limits component-wise, default 10*h0 */
-  int32_t use_pp;  /* apply M Pi (Alg. 3); default 0 when the struct is zero -- set 1 to enable */
+  int32_t use_pp;  /* apply M Pi (Alg. 3); fields are used as given (NULL params => both on) */
   int32_t use_tvb; /* apply Lambda Pi */
   int32_t device;  /* CUDA device ordinal */
   void *stream;    /* cudaStream_t for all work (e.g. torch.cuda.current_stream()), NULL = legacy default */
@@ -81,6 +81,20 @@ typedef struct {
   void *(*dev_alloc)(size_t bytes, void *stream, void *user);
   void (*dev_free)(void *ptr, void *stream, void *user);
   void *alloc_user;
+  /* Multi-GPU (element partition).  nranks <= 1: single rank, every
+   * element owned.  Otherwise every element of the given mesh carries an owner
+   * rank (owner[nelems]) and a global id (gid[nelems], NULL => the index; gids
+   * must agree across ranks for the elements the ranks share).  Each rank
+   * advances the elements it owns; the non-owned face neighbours of owned
+   * elements are ghosts refreshed by halo exchanges after every level update;
+   * elements that are neither are ignored.  Transport: NCCL when nccl_id
+   * (128-byte ncclUniqueId, same on all ranks, see swe_nccl_unique_id) is set;
+   * otherwise several contexts of one process are linked with swe_link_group
+   * and advanced with swe_step_group. */
+  int32_t rank, nranks;
+  const int32_t *owner;
+  const int64_t *gid;
+  const void *nccl_id;
 } swe_params;
 
 typedef struct {
@@ -126,6 +140,15 @@ int swe_get_state(swe_ctx *ctx, double *h, double *hu, double *hv);
 
 void swe_destroy(swe_ctx *ctx); /* NULL-safe; frees all device memory */
 
+/* ------------------------------------------------------------ multi-rank */
+/* A fresh NCCL unique id (128 bytes) for swe_params.nccl_id; call on one rank and broadcast. */
+int swe_nccl_unique_id(void *id128);
+/* Link n contexts of this process (ranks 0..n-1 of one partition, same device and stream) so that
+ * swe_step_group advances them together with in-process halo copies (one-GPU validation of the
+ * partitioned path).  swe_get_state / swe_get_info of a linked context materialise the group. */
+int swe_link_group(swe_ctx **ctxs, int n);
+int swe_step_group(swe_ctx **ctxs, int n, double dt, int nlevels);
+
 /* ------------------------------------------------------------ introspection */
 int swe_get_levels(swe_ctx *ctx, int32_t *level);                       /* [nelems], 1..nlevels */
 int swe_get_connectivity(const swe_ctx *ctx, int32_t *etoe, int8_t *etof); /* [nelems*3], boundary = self */
@@ -152,6 +175,11 @@ int swe_host_levels(const swe_mesh *mesh, int N, double g, const double *h, cons
                     const swe_params *params, int nlevels, int32_t *level);
 /* Static TVB geometry: pairs[K*3*2] (neighbour face slots used for edge i), alphas[K*3*2]. */
 int swe_host_tvb_geometry(const swe_mesh *mesh, int32_t *pairs, double *alphas);
+/* Halo plan of `rank`: counts = {owned, ghosts, npeers}; peers[3*i] = peer rank, [3*i+1] = send count,
+ * [3*i+2] = receive count; send_gids / recv_gids: the lists concatenated in peer order (gid order
+ * within a peer).  Any output pointer except counts may be NULL (query sizes first). */
+int swe_host_halo_plan(const swe_mesh *mesh, const int64_t *gid, const int32_t *owner, int rank, int32_t *counts,
+                       int32_t *peers, int64_t *send_gids, int64_t *recv_gids);
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,9 @@ SWE_ERRORS = {0: "SWE_OK", -1: "SWE_ERR_ARG", -2: "SWE_ERR_MESH", -3: "SWE_ERR_O
 
 EXPORTED = ["swe_nodes", "swe_create", "swe_set_state", "swe_step", "swe_get_state", "swe_destroy", "swe_get_levels",
             "swe_get_connectivity", "swe_get_info", "swe_last_error", "swe_profile", "swe_profile_read",
-            "swe_host_refel", "swe_host_connectivity", "swe_host_hk", "swe_host_levels", "swe_host_tvb_geometry"]
+            "swe_nccl_unique_id", "swe_link_group", "swe_step_group",
+            "swe_host_refel", "swe_host_connectivity", "swe_host_hk", "swe_host_levels", "swe_host_tvb_geometry",
+            "swe_host_halo_plan"]
 
 
 class SweError(RuntimeError):
@@ -44,7 +46,9 @@ class SweParams(C.Structure):
     _fields_ = [("h0", C.c_double), ("eps", C.c_double), ("tvb_M", C.c_double), ("tvb_nu", C.c_double),
                 ("a_floor", C.c_double), ("eps_u", C.c_double), ("h_char", C.c_double),
                 ("use_pp", C.c_int32), ("use_tvb", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
-                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", C.c_void_p)]
+                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", C.c_void_p),
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("owner", C.POINTER(C.c_int32)),
+                ("gid", C.POINTER(C.c_int64)), ("nccl_id", C.c_void_p)]
 
 
 class SweInfo(C.Structure):
@@ -91,6 +95,11 @@ def lib():
         L.swe_host_levels.argtypes = [C.POINTER(SweMesh), C.c_int, C.c_double, dp, dp, dp, C.POINTER(SweParams),
                                       C.c_int, ip]
         L.swe_host_tvb_geometry.argtypes = [C.POINTER(SweMesh), ip, dp]
+        L.swe_nccl_unique_id.argtypes = [C.c_void_p]
+        L.swe_link_group.argtypes = [C.POINTER(vp), C.c_int]
+        L.swe_step_group.argtypes = [C.POINTER(vp), C.c_int, C.c_double, C.c_int]
+        L.swe_host_halo_plan.argtypes = [C.POINTER(SweMesh), C.POINTER(C.c_int64), ip, C.c_int, ip, ip,
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         for n in EXPORTED:
             if n not in ("swe_destroy", "swe_last_error"):
                 getattr(L, n).restype = C.c_int
@@ -124,9 +133,17 @@ def _check(rc, ctx=None):
         raise SweError(rc, msg)
 
 
-def _params(p: dict | None, device=0, stream=None, alloc=None) -> SweParams:
+def _params(p: dict | None, device=0, stream=None, alloc=None, part=None) -> SweParams:
     p = dict(p or {})
     sp = SweParams()
+    sp.nranks = 1
+    if part is not None:
+        sp.rank, sp.nranks = int(part["rank"]), int(part["nranks"])
+        sp.owner = _p(part["owner"], C.c_int32)
+        if part.get("gid") is not None:
+            sp.gid = _p(part["gid"], C.c_int64)
+        if part.get("nccl_id") is not None:
+            sp.nccl_id = C.cast(part["nccl_id"], C.c_void_p)
     for k in ("h0", "eps", "tvb_M", "tvb_nu", "a_floor", "eps_u", "h_char"):
         setattr(sp, k, float(p.get(k, 0.0)))
     sp.use_pp = int(p.get("use_pp", 1))
@@ -182,6 +199,32 @@ def host_levels(vx, vy, etov, N, g, h, hu, hv, nlevels, params=None, vper=None):
     return lev
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().swe_nccl_unique_id(buf))
+    return buf.raw
+
+
+def host_halo_plan(vx, vy, etov, owner, rank, gid=None, vper=None):
+    """Halo plan of `rank` (host only): dict(owned, ghosts, peers=[(rank, nsend, nrecv)], send_gids, recv_gids)."""
+    m = _MeshArgs(vx, vy, etov, vper)
+    own = np.ascontiguousarray(owner, dtype=np.int32)
+    g = None if gid is None else np.ascontiguousarray(gid, dtype=np.int64)
+    gp = None if g is None else _p(g, C.c_int64)
+    cnt = np.zeros(3, dtype=np.int32)
+    _check(lib().swe_host_halo_plan(C.byref(m.s), gp, _p(own, C.c_int32), int(rank), _p(cnt, C.c_int32), None, None,
+                                    None))
+    peers = np.zeros((max(1, cnt[2]), 3), dtype=np.int32)
+    _check(lib().swe_host_halo_plan(C.byref(m.s), gp, _p(own, C.c_int32), int(rank), _p(cnt, C.c_int32),
+                                    _p(peers, C.c_int32), None, None))
+    ns, nr = int(peers[:cnt[2], 1].sum()), int(peers[:cnt[2], 2].sum())
+    sg, rg = np.zeros(max(1, ns), dtype=np.int64), np.zeros(max(1, nr), dtype=np.int64)
+    _check(lib().swe_host_halo_plan(C.byref(m.s), gp, _p(own, C.c_int32), int(rank), _p(cnt, C.c_int32),
+                                    _p(peers, C.c_int32), _p(sg, C.c_int64), _p(rg, C.c_int64)))
+    return {"owned": int(cnt[0]), "ghosts": int(cnt[1]), "peers": [tuple(map(int, r)) for r in peers[:cnt[2]]],
+            "send_gids": sg[:ns], "recv_gids": rg[:nr]}
+
+
 def host_tvb_geometry(vx, vy, etov, vper=None):
     m = _MeshArgs(vx, vy, etov, vper)
     pairs = np.zeros((m.K, 3, 2), dtype=np.int32)
@@ -215,7 +258,7 @@ class Solver:
     """One solver context (swe_create ... swe_destroy)."""
 
     def __init__(self, vx, vy, etov, B, N, g, vper=None, params: dict | None = None, device: int = 0,
-                 use_torch: bool = True):
+                 use_torch: bool = True, rank: int = 0, nranks: int = 1, owner=None, gid=None, nccl_id=None):
         L = lib()
         self._mesh = _MeshArgs(vx, vy, etov, vper)
         self.K = self._mesh.K
@@ -229,8 +272,14 @@ class Solver:
             torch.cuda.set_device(device)
             stream = C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
             self._alloc = _TorchAllocator(device)
+        self._part = None
+        if nranks > 1:
+            self._part = {"rank": rank, "nranks": nranks,
+                          "owner": np.ascontiguousarray(owner, dtype=np.int32),
+                          "gid": None if gid is None else np.ascontiguousarray(gid, dtype=np.int64),
+                          "nccl_id": None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)}
         self._sp = _params(params, device, stream,
-                           None if self._alloc is None else (self._alloc.alloc, self._alloc.free))
+                           None if self._alloc is None else (self._alloc.alloc, self._alloc.free), self._part)
         h = C.c_void_p()
         rc = L.swe_create(C.byref(self._mesh.s), _p(self._B), N, float(g), C.byref(self._sp), C.byref(h))
         if rc != 0:
@@ -295,3 +344,16 @@ class Solver:
         _check(lib().swe_profile_read(self._h, _p(t), _p(n, C.c_int64), _p(b)), self._h)
         return {"k1_ms": t[0], "k2_ms": t[1], "k1_launches": int(n[0]), "k2_launches": int(n[1]),
                 "k1_bytes": b[0], "k2_bytes": b[1]}
+
+
+def link_group(solvers):
+    """Link in-process solvers (ranks 0..n-1 of one partition, same device/stream)."""
+    arr = (C.c_void_p * len(solvers))(*[s._h for s in solvers])
+    _check(lib().swe_link_group(arr, len(solvers)))
+    return arr
+
+
+def step_group(solvers, dt, nlevels=1):
+    arr = (C.c_void_p * len(solvers))(*[s._h for s in solvers])
+    rc = lib().swe_step_group(arr, len(solvers), float(dt), int(nlevels))
+    _check(rc, solvers[0]._h)

@@ -13,6 +13,16 @@ LIB = os.path.join(HERE, "libswe_b200.so")
 BUILD = os.path.join(HERE, "_build")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dirs():
+    """NCCL headers/library: the copy torch loads (nvidia-nccl wheel), else the system one."""
+    try:
+        import nvidia.nccl as _n
+        base = list(_n.__path__)[0]
+        return os.path.join(base, "include"), os.path.join(base, "lib")
+    except Exception:
+        return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_SRC = ["refel.cpp", "mesh.cpp"]
 CU_SRC = ["solver.cu"]
@@ -42,12 +52,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")
         if force or _stale(obj, [src] + deps):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-I", _nccl_dirs()[0], "-Xcompiler", "-fPIC,-ffp-contract=off",
                    "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
             subprocess.check_call(cmd)
         objs.append(obj)
     if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart"]
+        inc, libdir = _nccl_dirs()
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart", "-L", libdir, "-l:libnccl.so.2",
+               "-Xlinker", "-rpath=" + libdir]
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
     return LIB

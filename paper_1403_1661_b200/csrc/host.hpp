@@ -65,8 +65,28 @@ void element_speeds(int K, int Np, double g, double eps_u, double a_floor, const
                     const double *hv, double *ae);
 // level = 1 + max{k in [0,L-1] : Hk/a_e >= 2^k r_min}  (reading A19)
 void bin_levels(int K, const double *hk, const double *ae, int L, int32_t *level);
+// same with a given (global, all-rank) r_min
+void bin_levels_rmin(int K, const double *hk, const double *ae, int L, double rmin, int32_t *level);
 
 // Internal element order: level-major, Morton order of the barycentres within a level.
 void element_order(const HostMesh &m, const int32_t *level, std::vector<int32_t> &order);
+
+}  // namespace swe
+
+namespace swe {
+
+// Partition of a (sub-)mesh among ranks.  Every element of the
+// given mesh carries a global id and an owner rank.  Owned elements are the
+// ones with owner == rank; ghosts are the non-owned face neighbours of owned
+// elements; every other element is dropped.  Send list to peer q: owned
+// elements with a ghost neighbour owned by q; receive list from q: ghosts owned
+// by q.  Both sides order their lists by global id, so rank r's send list to q
+// equals q's receive list from r element by element.
+struct HaloPlan {
+  std::vector<int32_t> owned, ghosts;   // element indices of the given mesh
+  std::vector<int32_t> peers;           // peer ranks, ascending
+  std::vector<std::vector<int32_t>> send, recv;  // per peer: element indices of the given mesh, by gid
+};
+void build_halo_plan(const HostMesh &m, const int64_t *gid, const int32_t *owner, int rank, HaloPlan &plan);
 
 }  // namespace swe

@@ -225,12 +225,18 @@ void element_speeds(int K, int Np, double g, double eps_u, double a_floor, const
 
 void bin_levels(int K, const double *hk, const double *ae, int L, int32_t *level) {
   const double inf = std::numeric_limits<double>::infinity();
-  std::vector<double> r(K);
   double rmin = inf;
   for (int e = 0; e < K; e++) {
-    r[e] = ae[e] > 0.0 ? hk[e] / ae[e] : inf;
-    if (r[e] < rmin) rmin = r[e];
+    double r = ae[e] > 0.0 ? hk[e] / ae[e] : inf;
+    if (r < rmin) rmin = r;
   }
+  bin_levels_rmin(K, hk, ae, L, rmin, level);
+}
+
+void bin_levels_rmin(int K, const double *hk, const double *ae, int L, double rmin, int32_t *level) {
+  const double inf = std::numeric_limits<double>::infinity();
+  std::vector<double> r(K);
+  for (int e = 0; e < K; e++) r[e] = ae[e] > 0.0 ? hk[e] / ae[e] : inf;
   for (int e = 0; e < K; e++) {
     int l = 1;
     for (int k = 1; k < L; k++)
@@ -273,6 +279,60 @@ void element_order(const HostMesh &m, const int32_t *level, std::vector<int32_t>
   std::sort(keys.begin(), keys.end());
   order.resize(K);
   for (int k = 0; k < K; k++) order[k] = keys[k].second;
+}
+
+}  // namespace swe
+
+namespace swe {
+
+void build_halo_plan(const HostMesh &m, const int64_t *gid, const int32_t *owner, int rank, HaloPlan &plan) {
+  const int K = m.K;
+  plan = HaloPlan();
+  std::vector<char> is_ghost(K, 0);
+  std::vector<std::vector<int32_t>> send_by_rank;
+  std::vector<int32_t> peer_slot;
+  auto slot_of = [&](int q) {
+    for (size_t i = 0; i < plan.peers.size(); i++)
+      if (plan.peers[i] == q) return (int)i;
+    plan.peers.push_back(q);
+    plan.send.push_back({});
+    plan.recv.push_back({});
+    return (int)plan.peers.size() - 1;
+  };
+  for (int e = 0; e < K; e++) {
+    if (owner[e] != rank) continue;
+    plan.owned.push_back(e);
+    std::vector<int> sent_to;
+    for (int f = 0; f < 3; f++) {
+      int n = m.etoe[(size_t)3 * e + f];
+      if (n == e || owner[n] == rank) continue;
+      if (!is_ghost[n]) {
+        is_ghost[n] = 1;
+        plan.ghosts.push_back(n);
+      }
+      int q = owner[n];
+      if (std::find(sent_to.begin(), sent_to.end(), q) == sent_to.end()) {
+        sent_to.push_back(q);
+        plan.send[slot_of(q)].push_back(e);
+      }
+    }
+  }
+  for (int g : plan.ghosts) plan.recv[slot_of(owner[g])].push_back(g);
+  // peers ascending, lists by global id
+  std::vector<size_t> ord(plan.peers.size());
+  for (size_t i = 0; i < ord.size(); i++) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return plan.peers[a] < plan.peers[b]; });
+  HaloPlan sorted = plan;
+  for (size_t i = 0; i < ord.size(); i++) {
+    sorted.peers[i] = plan.peers[ord[i]];
+    sorted.send[i] = plan.send[ord[i]];
+    sorted.recv[i] = plan.recv[ord[i]];
+  }
+  plan = sorted;
+  auto by_gid = [&](int32_t a, int32_t b) { return gid[a] < gid[b]; };
+  for (auto &v : plan.send) std::sort(v.begin(), v.end(), by_gid);
+  for (auto &v : plan.recv) std::sort(v.begin(), v.end(), by_gid);
+  std::sort(plan.ghosts.begin(), plan.ghosts.end(), by_gid);
 }
 
 }  // namespace swe

@@ -2,10 +2,12 @@
 // B200-native DG shallow-water solver.  Device work: kernels.cuh (hot path)
 // plus the setup / permutation / diagnostics kernels below.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -61,7 +63,8 @@ __global__ void k_scatter_field(int K, int Np, const int *orig, const double *sr
 
 // internal committed state (parity per level) -> caller layout
 struct GatherParams {
-  int K, Np, nlev, off[9], par[8];
+  int K, Np, nlev, off[9], par[8];  // K = elements to process (owned), Kstride = array stride
+  int Kstride;
   const int *orig;
   const double *Q;
   double *h, *hu, *hv;
@@ -71,7 +74,7 @@ __global__ void k_gather_state(const __grid_constant__ GatherParams p) {
   if (k >= p.K) return;
   int c = 0;
   for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
-  const size_t K = p.K;
+  const size_t K = p.Kstride;
   const double *Q = p.Q + (size_t)p.par[c] * 3 * p.Np * K;
   size_t e = (size_t)p.orig[k];
   for (int i = 0; i < p.Np; i++) {
@@ -90,7 +93,7 @@ __global__ void k_diag(const __grid_constant__ GatherParams p, const double *V, 
   if (k < p.K) {
     int c = 0;
     for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
-    const size_t K = p.K;
+    const size_t K = p.Kstride;
     const double *Q = p.Q + (size_t)p.par[c] * 3 * p.Np * K;
     double x0 = V[k], x1 = V[K + k], x2 = V[2 * K + k], y0 = V[3 * K + k], y1 = V[4 * K + k], y2 = V[5 * K + k];
     double J = 0.25 * ((x1 - x0) * (y2 - y0) - (x2 - x0) * (y1 - y0));
@@ -119,21 +122,43 @@ __global__ void k_diag(const __grid_constant__ GatherParams p, const double *V, 
 }
 
 // ------------------------------------------------------------------ context
+struct Ctx;
+
+// One exchange table per level: entries [level][peer] (send: owned boundary
+// elements, recv: ghosts), each peer's list in global-id order.
+struct XTable {
+  std::vector<int> cnt;  // [(L+1) * npeer]  (level 1..L)
+  std::vector<int> off;  // start of (level, peer) within the flattened index array
+  std::vector<int> loff; // start of level l block: loff[l-1] .. loff[l]
+  int total = 0;
+};
+
 struct Ctx {
   std::string err;
-  int N = 0, Np = 0, K = 0, device = 0;
+  int N = 0, Np = 0, device = 0;
+  int Kin = 0;   // elements of the mesh given to swe_create
+  int K = 0;     // local elements (owned + ghosts)
+  int kown = 0;  // owned elements
+  int rank = 0, nranks = 1;
   double g = 9.81;
   swe_params prm;
   cudaStream_t stream = 0;
   RefOps ops;
-  HostMesh mesh;
+  HostMesh mesh;  // given mesh, with connectivity
   TvbGeom tvb;
-  std::vector<double> Bcaller;  // host copy (caller layout)
+  std::vector<int64_t> gid;
+  std::vector<int32_t> owner;
+  HaloPlan plan;  // peers / send / recv lists (given-mesh indices)
+  // transport
+  ncclComm_t comm = nullptr;
+  std::vector<Ctx *> group;  // in-process peers (local transport), indexed by rank
   // device
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
   double *dTalpha = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
-  double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr;
-  int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr;
+  double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dRmin = nullptr;
+  double *dXsBuf = nullptr, *dXrBuf = nullptr;
+  int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
+  size_t xcap = 0;  // capacity (entries) of the exchange index/buffer arrays
   unsigned char *dDry = nullptr;
   unsigned long long *dCounters = nullptr;
   unsigned long long *hCounters = nullptr;  // pinned
@@ -142,18 +167,19 @@ struct Ctx {
   bool have_state = false, materialized = false, scheduled = false;
   double dt = 0.0;
   int L = 1;
-  std::vector<int32_t> level;      // caller order
-  std::vector<int32_t> order;      // internal k -> caller e
-  int off[9] = {0};
+  std::vector<int32_t> level;  // given-mesh order
+  std::vector<int32_t> order;  // internal k -> given-mesh e (owned first, then ghosts)
+  int off[9] = {0}, goff[9] = {0};
+  XTable xs, xr;
   int kcount[9] = {0}, par[9] = {0};
   long tick_s[9] = {0}, t_e[9] = {0};
   long tick = 0;
   long n_updates = 0;
   std::vector<std::pair<int, long>> schedule;  // (level, tick offset) of one macro step
+  StepParams cur;  // parameters of the update in flight
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;
-  std::vector<int> ev_kind;
   double prof_ms[2] = {0, 0}, prof_bytes[2] = {0, 0};
   long prof_launch[2] = {0, 0};
   bool alloc_ok = true;
@@ -186,6 +212,14 @@ static int cuda_fail(Ctx *c, cudaError_t e, const char *where) {
   do {                                                    \
     cudaError_t _e = (call);                              \
     if (_e != cudaSuccess) return cuda_fail(c, _e, #call); \
+  } while (0)
+#define NK(call)                                                           \
+  do {                                                                     \
+    ncclResult_t _r = (call);                                              \
+    if (_r != ncclSuccess) {                                               \
+      c->err = std::string(#call) + ": " + ncclGetErrorString(_r);         \
+      return SWE_ERR_NCCL;                                                 \
+    }                                                                      \
   } while (0)
 
 template <int N>
@@ -324,13 +358,17 @@ static StepParams base_params(Ctx *c) {
   p.injected = c->dInjected;
   p.opsG = c->dOpsG;
   p.nlev = c->L;
-  for (int l = 0; l <= 8; l++) p.off[l] = c->off[l];
+  p.kown = c->kown;
+  for (int l = 0; l <= 8; l++) {
+    p.off[l] = c->off[l];
+    p.goff[l] = c->goff[l];
+  }
   return p;
 }
 
 static int alloc_state(Ctx *c) {
   if (c->dQ) return SWE_OK;
-  size_t K = c->K, Np = c->Np;
+  size_t K = c->K, Np = c->Np, Kin = c->Kin;
   c->dQ = (double *)c->dalloc(sizeof(double) * 2 * 3 * Np * K);
   c->dR = (double *)c->dalloc(sizeof(double) * 3 * 3 * Np * K);
   c->dB = (double *)c->dalloc(sizeof(double) * Np * K);
@@ -338,13 +376,22 @@ static int alloc_state(Ctx *c) {
   c->dMeans = (double *)c->dalloc(sizeof(double) * 3 * K);
   c->dUT = (double *)c->dalloc(sizeof(double) * 9 * K);
   c->dTalpha = (double *)c->dalloc(sizeof(double) * 6 * K);
-  c->dAe = (double *)c->dalloc(sizeof(double) * K);
-  c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * K);
+  c->dAe = (double *)c->dalloc(sizeof(double) * Kin);
+  c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * Kin);
   c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
   c->dTcode = (int *)c->dalloc(sizeof(int) * K);
   c->dOrig = (int *)c->dalloc(sizeof(int) * K);
   c->dDry = (unsigned char *)c->dalloc(K);
   c->dPartials = (double *)c->dalloc(sizeof(double) * 2 * ((K + 255) / 256));
+  c->dRmin = (double *)c->dalloc(sizeof(double));
+  size_t ns = 0, nr = 0;
+  for (auto &v : c->plan.send) ns += v.size();
+  for (auto &v : c->plan.recv) nr += v.size();
+  c->xcap = std::max(ns, nr) + 1;
+  c->dXsIdx = (int *)c->dalloc(sizeof(int) * c->xcap);
+  c->dXrIdx = (int *)c->dalloc(sizeof(int) * c->xcap);
+  c->dXsBuf = (double *)c->dalloc(sizeof(double) * 6 * Np * c->xcap);
+  c->dXrBuf = (double *)c->dalloc(sizeof(double) * 6 * Np * c->xcap);
   if (!c->alloc_ok) {
     c->err = "device allocation failed";
     return SWE_ERR_NOMEM;
@@ -352,33 +399,182 @@ static int alloc_state(Ctx *c) {
   return SWE_OK;
 }
 
-// Build the internal element order for `levels`, upload the static data in
-// that order, scatter the staged (unlimited) state, apply Alg. 2 line 1
-// (M Pi then Lambda Pi on all elements) and reset the MRAB schedule.
+// Exchange tables for the current internal order: entries [level][peer].
+static void build_xtable(Ctx *c, const std::vector<std::vector<int32_t>> &lists, const std::vector<int32_t> &inv,
+                         XTable &t, std::vector<int> &flat) {
+  const int np = (int)c->plan.peers.size(), L = c->L;
+  t.cnt.assign((size_t)(L + 1) * std::max(np, 1), 0);
+  t.off.assign((size_t)(L + 1) * std::max(np, 1), 0);
+  t.loff.assign(L + 2, 0);
+  flat.clear();
+  for (int l = 1; l <= L; l++) {
+    t.loff[l - 1] = (int)flat.size();
+    for (int i = 0; i < np; i++) {
+      t.off[(size_t)l * np + i] = (int)flat.size();
+      for (int e : lists[i])
+        if (c->level[e] == l) flat.push_back(inv[e]);
+      t.cnt[(size_t)l * np + i] = (int)flat.size() - t.off[(size_t)l * np + i];
+    }
+  }
+  t.loff[L] = (int)flat.size();
+  t.total = (int)flat.size();
+}
+
+// ------------------------------------------------------------------ halo exchange (pack / transfer / unpack)
+static int payload(Ctx *c, int phase) { return phase == 0 ? 4 : 6 * c->Np; }
+
+// lvl = 0: all levels (initial exchange), else one level
+static int xpack(Ctx *c, int phase, int lvl, int par, int slot) {
+  if (c->plan.peers.empty()) return SWE_OK;
+  int a = lvl == 0 ? 0 : c->xs.loff[lvl - 1], b = lvl == 0 ? c->xs.total : c->xs.loff[lvl];
+  if (b <= a) return SWE_OK;
+  HaloParams h;
+  std::memset(&h, 0, sizeof(h));
+  h.n = b - a;
+  h.K = c->K;
+  h.Np = c->Np;
+  h.phase = phase;
+  h.par = par;
+  h.slot = slot;
+  h.idx = c->dXsIdx + a;
+  h.buf = c->dXsBuf + (size_t)payload(c, phase) * a;
+  h.Q = c->dQ;
+  h.R = c->dR;
+  h.means = c->dMeans;
+  h.dry = c->dDry;
+  k_halo_pack<<<(h.n + 127) / 128, 128, 0, c->stream>>>(h);
+  CK(cudaGetLastError());
+  return SWE_OK;
+}
+
+static int xunpack(Ctx *c, int phase, int lvl, int par, int slot) {
+  if (c->plan.peers.empty()) return SWE_OK;
+  int a = lvl == 0 ? 0 : c->xr.loff[lvl - 1], b = lvl == 0 ? c->xr.total : c->xr.loff[lvl];
+  if (b <= a) return SWE_OK;
+  HaloParams h;
+  std::memset(&h, 0, sizeof(h));
+  h.n = b - a;
+  h.K = c->K;
+  h.Np = c->Np;
+  h.phase = phase;
+  h.par = par;
+  h.slot = slot;
+  h.idx = c->dXrIdx + a;
+  h.buf = c->dXrBuf + (size_t)payload(c, phase) * a;
+  h.Q = c->dQ;
+  h.R = c->dR;
+  h.means = c->dMeans;
+  h.dry = c->dDry;
+  k_halo_unpack<<<(h.n + 127) / 128, 128, 0, c->stream>>>(h);
+  CK(cudaGetLastError());
+  return SWE_OK;
+}
+
+// transfer: NCCL point-to-point (one group per exchange) or in-process peers
+static int xtransfer(Ctx *c, int phase, int lvl) {
+  const int np = (int)c->plan.peers.size();
+  if (np == 0) return SWE_OK;
+  const int P = payload(c, phase);
+  if (c->comm) {
+    NK(ncclGroupStart());
+    for (int i = 0; i < np; i++) {
+      for (int l = (lvl == 0 ? 1 : lvl); l <= (lvl == 0 ? c->L : lvl); l++) {
+        int so = c->xs.off[(size_t)l * np + i], sc = c->xs.cnt[(size_t)l * np + i];
+        int ro = c->xr.off[(size_t)l * np + i], rc = c->xr.cnt[(size_t)l * np + i];
+        if (sc > 0) NK(ncclSend(c->dXsBuf + (size_t)P * so, (size_t)P * sc, ncclDouble, c->plan.peers[i], c->comm, c->stream));
+        if (rc > 0) NK(ncclRecv(c->dXrBuf + (size_t)P * ro, (size_t)P * rc, ncclDouble, c->plan.peers[i], c->comm, c->stream));
+      }
+    }
+    NK(ncclGroupEnd());
+    return SWE_OK;
+  }
+  if (!c->group.empty()) {  // in-process peers on one device: copy out of the peer's send buffer
+    for (int i = 0; i < np; i++) {
+      Ctx *q = c->group[c->plan.peers[i]];
+      int qi = -1;
+      for (size_t j = 0; j < q->plan.peers.size(); j++)
+        if (q->plan.peers[j] == c->rank) qi = (int)j;
+      if (qi < 0) {
+        c->err = "halo plan mismatch between in-process peers";
+        return SWE_ERR_STATE;
+      }
+      const int qnp = (int)q->plan.peers.size();
+      for (int l = (lvl == 0 ? 1 : lvl); l <= (lvl == 0 ? c->L : lvl); l++) {
+        int ro = c->xr.off[(size_t)l * np + i], rc = c->xr.cnt[(size_t)l * np + i];
+        int so = q->xs.off[(size_t)l * qnp + qi], sc = q->xs.cnt[(size_t)l * qnp + qi];
+        if (rc != sc) {
+          c->err = "halo exchange size mismatch";
+          return SWE_ERR_STATE;
+        }
+        if (rc > 0)
+          CK(cudaMemcpyAsync(c->dXrBuf + (size_t)P * ro, q->dXsBuf + (size_t)P * so, sizeof(double) * P * rc,
+                             cudaMemcpyDeviceToDevice, c->stream));
+      }
+    }
+    return SWE_OK;
+  }
+  c->err = "ranks > 1 without a transport (pass nccl_id or use swe_step_group)";
+  return SWE_ERR_NCCL;
+}
+
+// Element order for a subset: level-major, Morton within a level (owned elements).
+static void order_subset(const HostMesh &m, const std::vector<int32_t> &levels, const std::vector<int32_t> &subset,
+                         std::vector<int32_t> &out) {
+  std::vector<int32_t> all;
+  element_order(m, levels.data(), all);  // global level-major Morton order
+  std::vector<char> in(m.K, 0);
+  for (int e : subset) in[e] = 1;
+  out.clear();
+  for (int e : all)
+    if (in[e]) out.push_back(e);
+}
+
+// Build the internal order for `levels` (given-mesh order), upload static data,
+// scatter the staged unlimited state, reset the MRAB schedule.  The initial
+// limiting (Alg. 2 line 1) is applied by init_limit_* (group-aware).
 static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   const int K = c->K;
-  element_order(c->mesh, levels.data(), c->order);
-  for (int k = 1; k < K; k++)
+  c->level = levels;
+  c->L = L;
+  std::vector<int32_t> owned_sorted, ghosts_sorted;
+  order_subset(c->mesh, levels, c->plan.owned, owned_sorted);
+  ghosts_sorted = c->plan.ghosts;
+  std::stable_sort(ghosts_sorted.begin(), ghosts_sorted.end(), [&](int a, int b) {
+    if (levels[a] != levels[b]) return levels[a] < levels[b];
+    return c->gid[a] < c->gid[b];
+  });
+  c->order = owned_sorted;
+  c->order.insert(c->order.end(), ghosts_sorted.begin(), ghosts_sorted.end());
+  if ((int)c->order.size() != K) {
+    c->err = "local element count mismatch";
+    return SWE_ERR_STATE;
+  }
+  for (int k = 1; k < c->kown; k++)
     if (levels[c->order[k]] < levels[c->order[k - 1]]) {
       c->err = "internal element order is not level-major";
       return SWE_ERR_SCHEDULE;
     }
-  std::vector<int32_t> inv(K);
+  std::vector<int32_t> inv(c->Kin, -1);
   for (int k = 0; k < K; k++) inv[c->order[k]] = k;
-  for (int l = 0; l <= 8; l++) c->off[l] = K;
-  c->off[0] = 0;
-  {
-    std::vector<int> cnt(10, 0);
-    for (int e = 0; e < K; e++) cnt[levels[e]]++;
-    int acc = 0;
-    for (int l = 1; l <= L; l++) {
-      c->off[l - 1] = acc;
-      acc += cnt[l];
-    }
-    for (int l = L; l <= 8; l++) c->off[l] = K;
+  // level offsets (owned, then ghosts)
+  for (int l = 0; l <= 8; l++) {
+    c->off[l] = c->kown;
+    c->goff[l] = K;
   }
-  std::vector<double> V((size_t)6 * K), TA((size_t)6 * K);
-  std::vector<int> E2E((size_t)3 * K), TC(K);
+  {
+    std::vector<int> co(10, 0), cg(10, 0);
+    for (int k = 0; k < c->kown; k++) co[levels[c->order[k]]]++;
+    for (int k = c->kown; k < K; k++) cg[levels[c->order[k]]]++;
+    int ao = 0, ag = c->kown;
+    for (int l = 1; l <= L; l++) {
+      c->off[l - 1] = ao;
+      c->goff[l - 1] = ag;
+      ao += co[l];
+      ag += cg[l];
+    }
+  }
+  std::vector<double> V((size_t)6 * K, 0.0), TA((size_t)6 * K, 0.0);
+  std::vector<int> E2E((size_t)3 * K), TC(K, 0);
   for (int k = 0; k < K; k++) {
     int e = c->order[k];
     const int32_t *v = &c->mesh.etov[(size_t)3 * e];
@@ -389,7 +585,15 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
     int code = 0;
     for (int f = 0; f < 3; f++) {
       int n = c->mesh.etoe[(size_t)3 * e + f], nf = c->mesh.etof[(size_t)3 * e + f];
-      E2E[(size_t)f * K + k] = (inv[n] << 2) | nf;
+      if (k < c->kown) {
+        if (inv[n] < 0) {
+          c->err = "owned element with a neighbour outside the local set";
+          return SWE_ERR_MESH;
+        }
+        E2E[(size_t)f * K + k] = (inv[n] << 2) | nf;
+      } else {
+        E2E[(size_t)f * K + k] = (k << 2) | f;  // ghosts are never launched
+      }
       size_t s = (size_t)3 * e + f;
       code |= (c->tvb.pj[s] & 3) << (4 * f);
       code |= (c->tvb.pk[s] & 3) << (4 * f + 2);
@@ -398,24 +602,29 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
     }
     TC[k] = code;
   }
+  std::vector<int> xsf, xrf;
+  build_xtable(c, c->plan.send, inv, c->xs, xsf);
+  build_xtable(c, c->plan.recv, inv, c->xr, xrf);
   CK(cudaMemcpyAsync(c->dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dTalpha, TA.data(), sizeof(double) * TA.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dE2E, E2E.data(), sizeof(int) * E2E.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dTcode, TC.data(), sizeof(int) * TC.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dOrig, c->order.data(), sizeof(int) * K, cudaMemcpyHostToDevice, c->stream));
+  if (!xsf.empty())
+    CK(cudaMemcpyAsync(c->dXsIdx, xsf.data(), sizeof(int) * xsf.size(), cudaMemcpyHostToDevice, c->stream));
+  if (!xrf.empty())
+    CK(cudaMemcpyAsync(c->dXrIdx, xrf.data(), sizeof(int) * xrf.size(), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // host vectors above are released on return
   int nb = (K + 127) / 128;
   k_scatter_field<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dBcaller, c->dB);
-  const size_t KNp = (size_t)K * c->Np;
+  const size_t KNp = (size_t)c->Kin * c->Np;
   k_scatter_state<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp, c->dStage + 2 * KNp,
                                              c->dQ);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
-  // counters count from the (re-)application of Alg. 2 line 1
   CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream));
   CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream));
   c->n_updates = 0;
-  // schedule reset
-  c->L = L;
   for (int l = 0; l <= 8; l++) {
     c->kcount[l] = 0;
     c->par[l] = 0;
@@ -423,17 +632,6 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
     c->t_e[l] = 0;
   }
   c->tick = 0;
-  // Alg. 2 line 1: M Pi then Lambda Pi on every element, in place in Q[0]
-  StepParams p = base_params(c);
-  p.k0 = 0;
-  p.k1 = K;
-  p.nlev = 1;
-  for (int l = 1; l <= 8; l++) p.off[l] = K;
-  p.own_par = 0;
-  p.write_par = 0;
-  launch(0, true, c->N, p, c->stream);
-  if (c->prm.use_tvb) launch(1, false, c->N, p, c->stream);
-  CK(cudaGetLastError());
   c->materialized = true;
   return SWE_OK;
 }
@@ -477,7 +675,8 @@ static void dense_weights(int m, double th, double b[3]) {
   }
 }
 
-static int run_update(Ctx *c, int l, long t) {
+// Parameters of update (l, t) for one context (MRAB bookkeeping, reading A17).
+static StepParams update_params(Ctx *c, int l, long t) {
   StepParams p = base_params(c);
   p.k0 = c->off[l - 1];
   p.k1 = c->off[l];
@@ -518,61 +717,207 @@ static int run_update(Ctx *c, int l, long t) {
       }
     }
   }
+  return p;
+}
+
+static void launch_timed(Ctx *c, int which, const StepParams &p) {
   const int nel = p.k1 - p.k0;
-  if (c->prof && nel > 0) {
-    size_t i0 = c->ev.size();
-    for (int j = 0; j < 4; j++) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
-      c->ev.push_back(e);
-    }
-    cudaEventRecord(c->ev[i0], c->stream);
-    launch(0, false, c->N, p, c->stream);
-    cudaEventRecord(c->ev[i0 + 1], c->stream);
-    c->prof_bytes[0] += k1_bytes(c->N, m, c->prm.use_tvb) * nel;
-    c->prof_launch[0]++;
-    if (c->prm.use_tvb) {
-      cudaEventRecord(c->ev[i0 + 2], c->stream);
-      launch(1, false, c->N, p, c->stream);
-      cudaEventRecord(c->ev[i0 + 3], c->stream);
-      c->prof_bytes[1] += k2_bytes() * nel;
-      c->prof_launch[1]++;
-    } else {
-      cudaEventRecord(c->ev[i0 + 2], c->stream);
-      cudaEventRecord(c->ev[i0 + 3], c->stream);
-    }
+  if (nel <= 0) return;
+  if (c->prof) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->stream);
+    launch(which, false, c->N, p, c->stream);
+    cudaEventRecord(e1, c->stream);
+    c->ev.push_back(e0);
+    c->ev.push_back(e1);
+    c->prof_bytes[which] += (which == 0 ? k1_bytes(c->N, p.nab, c->prm.use_tvb) : k2_bytes()) * nel;
+    c->prof_launch[which]++;
   } else {
-    launch(0, false, c->N, p, c->stream);
-    if (c->prm.use_tvb) launch(1, false, c->N, p, c->stream);
+    launch(which, false, c->N, p, c->stream);
   }
-  c->n_updates += nel;
-  c->par[l] ^= 1;
-  c->kcount[l] = k + 1;
-  c->tick_s[l] = t;
-  c->t_e[l] = t + (1L << (l - 1));
-  return SWE_OK;
 }
 
 static void collect_profile(Ctx *c) {
-  for (size_t i = 0; i + 3 < c->ev.size(); i += 4) {
-    float a = 0, b = 0;
-    cudaEventElapsedTime(&a, c->ev[i], c->ev[i + 1]);
-    cudaEventElapsedTime(&b, c->ev[i + 2], c->ev[i + 3]);
-    c->prof_ms[0] += a;
-    c->prof_ms[1] += b;
+  // events come in (start, stop) pairs, K1 and K2 interleaved in launch order
+  for (size_t i = 0; i + 1 < c->ev.size(); i += 2) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
+    int which = (int)((i / 2) % (c->prm.use_tvb ? 2 : 1));
+    c->prof_ms[which] += ms;
   }
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   c->ev.clear();
 }
 
+// One MRAB update of level l at tick t for every context of the group, with
+// the two halo exchanges: A (means, dry; after K1) and B (Q, R slot; after K2).
+static int group_update(std::vector<Ctx *> &G, int l, long t) {
+  for (Ctx *c : G) {
+    c->cur = update_params(c, l, t);
+    launch_timed(c, 0, c->cur);
+  }
+  for (Ctx *c : G)
+    if (int rc = xpack(c, 0, l, 0, 0)) return rc;
+  for (Ctx *c : G)
+    if (int rc = xtransfer(c, 0, l)) return rc;
+  for (Ctx *c : G)
+    if (int rc = xunpack(c, 0, l, 0, 0)) return rc;
+  for (Ctx *c : G)
+    if (c->prm.use_tvb) launch_timed(c, 1, c->cur);
+  for (Ctx *c : G)
+    if (int rc = xpack(c, 1, l, c->cur.write_par, c->cur.write_slot)) return rc;
+  for (Ctx *c : G)
+    if (int rc = xtransfer(c, 1, l)) return rc;
+  for (Ctx *c : G)
+    if (int rc = xunpack(c, 1, l, c->cur.write_par, c->cur.write_slot)) return rc;
+  for (Ctx *c : G) {
+    c->n_updates += c->cur.k1 - c->cur.k0;
+    c->par[l] ^= 1;
+    c->kcount[l] = c->kcount[l] + 1;
+    c->tick_s[l] = t;
+    c->t_e[l] = t + (1L << (l - 1));
+  }
+  return SWE_OK;
+}
+
+// Alg. 2 line 1 on every owned element, then the full halo exchange.
+static int group_init_limit(std::vector<Ctx *> &G) {
+  for (Ctx *c : G) {
+    StepParams p = base_params(c);
+    p.k0 = 0;
+    p.k1 = c->kown;
+    p.own_par = 0;
+    p.write_par = 0;
+    c->cur = p;
+    launch(0, true, c->N, p, c->stream);
+    CK(cudaGetLastError());
+  }
+  for (Ctx *c : G)
+    if (int rc = xpack(c, 0, 0, 0, 0)) return rc;
+  for (Ctx *c : G)
+    if (int rc = xtransfer(c, 0, 0)) return rc;
+  for (Ctx *c : G)
+    if (int rc = xunpack(c, 0, 0, 0, 0)) return rc;
+  for (Ctx *c : G)
+    if (c->prm.use_tvb) launch(1, false, c->N, c->cur, c->stream);
+  for (Ctx *c : G)
+    if (int rc = xpack(c, 1, 0, 0, -1)) return rc;
+  for (Ctx *c : G)
+    if (int rc = xtransfer(c, 1, 0)) return rc;
+  for (Ctx *c : G)
+    if (int rc = xunpack(c, 1, 0, 0, -1)) return rc;
+  return SWE_OK;
+}
+
+// r_min over all ranks (levels are global, reading A19)
+static int group_bin(std::vector<Ctx *> &G, int nlevels) {
+  const double inf = std::numeric_limits<double>::infinity();
+  std::vector<std::vector<double>> ae(G.size());
+  double rmin = inf;
+  for (size_t i = 0; i < G.size(); i++) {
+    Ctx *c = G[i];
+    ae[i].resize(c->Kin);
+    CK(cudaMemcpyAsync(ae[i].data(), c->dAe, sizeof(double) * c->Kin, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int e = 0; e < c->Kin; e++) {
+      double r = ae[i][e] > 0.0 ? c->mesh.hk[e] / ae[i][e] : inf;
+      if (r < rmin) rmin = r;
+    }
+  }
+  if (G.size() == 1 && G[0]->comm) {  // global minimum across NCCL ranks
+    Ctx *c = G[0];
+    CK(cudaMemcpyAsync(c->dRmin, &rmin, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    NK(ncclAllReduce(c->dRmin, c->dRmin, 1, ncclDouble, ncclMin, c->comm, c->stream));
+    CK(cudaMemcpyAsync(&rmin, c->dRmin, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  for (size_t i = 0; i < G.size(); i++) {
+    Ctx *c = G[i];
+    std::vector<int32_t> lev(c->Kin, 1);
+    bin_levels_rmin(c->Kin, c->mesh.hk.data(), ae[i].data(), nlevels, rmin, lev.data());
+    if (int rc = materialize(c, lev, nlevels)) return rc;
+  }
+  return group_init_limit(G);
+}
+
+static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
+  for (Ctx *c : G) {
+    if (!c->have_state) {
+      c->err = "swe_step before swe_set_state";
+      return SWE_ERR_STATE;
+    }
+    if (!(dt > 0) || !std::isfinite(dt) || nlevels < 1 || nlevels > 8) {
+      c->err = "invalid dt or nlevels";
+      return SWE_ERR_ARG;
+    }
+  }
+  if (!G[0]->scheduled) {
+    if (int rc = group_bin(G, nlevels)) return rc;
+    for (Ctx *c : G) {
+      c->scheduled = true;
+      c->dt = dt;
+      c->L = nlevels;
+      c->schedule.clear();
+      build_schedule(nlevels, 0, c->schedule);
+    }
+  } else {
+    for (Ctx *c : G)
+      if (dt != c->dt || nlevels != c->L) {
+        c->err = "(dt, nlevels) differ from the first swe_step (levels are fixed, P:149)";
+        return SWE_ERR_SCHEDULE;
+      }
+  }
+  Ctx *c0 = G[0];
+  for (auto &st : c0->schedule)
+    if (int rc = group_update(G, st.first, c0->tick + st.second)) return rc;
+  for (Ctx *c : G) {
+    c->tick += 1L << (c->L - 1);
+    Ctx *c_ = c;
+    {
+      Ctx *c = c_;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost,
+                         c->stream));
+    }
+  }
+  for (Ctx *c : G) {
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->prof) collect_profile(c);
+    if (c->hCounters[3] != 0) {
+      c->err = "non-finite values produced";
+      return SWE_ERR_NONFINITE;
+    }
+  }
+  return SWE_OK;
+}
+
+static int ensure_materialized_group(std::vector<Ctx *> &G) {
+  bool need = false;
+  for (Ctx *c : G) need = need || !c->materialized;
+  if (!need) return SWE_OK;
+  for (Ctx *c : G) {
+    std::vector<int32_t> ones(c->Kin, 1);
+    if (int rc = materialize(c, ones, 1)) return rc;
+  }
+  return group_init_limit(G);
+}
+
+static std::vector<Ctx *> group_of(Ctx *c) {
+  if (c->group.empty()) return {c};
+  return c->group;
+}
+
 static GatherParams gather_params(Ctx *c, double *h, double *hu, double *hv) {
   GatherParams g;
   std::memset(&g, 0, sizeof(g));
-  g.K = c->K;
+  g.K = c->kown;  // owned elements only
   g.Np = c->Np;
   g.nlev = c->L;
   for (int l = 0; l <= 8; l++) g.off[l] = c->off[l];
   for (int l = 1; l <= 8; l++) g.par[l - 1] = c->par[l];
+  g.Kstride = c->K;
   g.orig = c->dOrig;
   g.Q = c->dQ;
   g.h = h;
@@ -606,6 +951,7 @@ static void fill_defaults(swe_params &p, const swe_params *in) {
   if (!(p.h_char > 0)) p.h_char = 10.0 * p.h0;
   if (p.a_floor < 0) p.a_floor = 0;
   if (p.tvb_M < 0) p.tvb_M = 0;
+  if (p.nranks < 1) p.nranks = 1;
 }
 
 int swe_nodes(const swe_mesh *mesh, int N, double *x, double *y) {
@@ -629,6 +975,14 @@ int swe_nodes(const swe_mesh *mesh, int N, double *x, double *y) {
   return SWE_OK;
 }
 
+int swe_nccl_unique_id(void *id128) {
+  if (!id128) return SWE_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SWE_ERR_NCCL;
+  std::memcpy(id128, &id, sizeof(id));
+  return SWE_OK;
+}
+
 int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe_params *params, swe_ctx **out) {
   if (!out) return SWE_ERR_ARG;
   *out = nullptr;
@@ -640,14 +994,17 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   fill_defaults(c->prm, params);
   c->N = N;
   c->Np = (N + 1) * (N + 2) / 2;
-  c->K = mesh->nelems;
+  c->Kin = mesh->nelems;
   c->g = g;
   c->device = c->prm.device;
   c->stream = (cudaStream_t)c->prm.stream;
+  c->rank = c->prm.rank;
+  c->nranks = c->prm.nranks;
   auto fail = [&](int rc) {
     swe_destroy(h);
     return rc;
   };
+  if (c->rank < 0 || c->rank >= c->nranks) return fail(SWE_ERR_ARG);
   int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, c->mesh, &c->err);
   if (rc) return fail(rc);
   if (!build_refops(N, c->ops, &c->err)) return fail(SWE_ERR_ORDER);
@@ -658,6 +1015,26 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
         return fail(SWE_ERR_ORDER);
       }
   build_tvb_geometry(c->mesh, c->tvb);
+  // ownership (every element owned by this rank when no partition is given)
+  c->gid.resize(c->Kin);
+  c->owner.assign(c->Kin, c->rank);
+  for (int e = 0; e < c->Kin; e++) c->gid[e] = c->prm.gid ? c->prm.gid[e] : e;
+  if (c->prm.owner) {
+    for (int e = 0; e < c->Kin; e++) {
+      if (c->prm.owner[e] < 0 || c->prm.owner[e] >= c->nranks) {
+        c->err = "owner rank out of range";
+        return fail(SWE_ERR_ARG);
+      }
+      c->owner[e] = c->prm.owner[e];
+    }
+  }
+  build_halo_plan(c->mesh, c->gid.data(), c->owner.data(), c->rank, c->plan);
+  c->kown = (int)c->plan.owned.size();
+  c->K = c->kown + (int)c->plan.ghosts.size();
+  if (c->kown == 0) {
+    c->err = "rank owns no element";
+    return fail(SWE_ERR_MESH);
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     c->err = "no CUDA device";
@@ -668,7 +1045,7 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   if (upload_ops_any(c->ops) != cudaSuccess) return fail(SWE_ERR_CUDA);
   rc = alloc_state(c);
   if (rc) return fail(rc);
-  c->dBcaller = (double *)c->dalloc(sizeof(double) * (size_t)c->K * c->Np);
+  c->dBcaller = (double *)c->dalloc(sizeof(double) * (size_t)c->Kin * c->Np);
   c->dWm2 = (double *)c->dalloc(sizeof(double) * c->Np);
   std::vector<double> sops = smem_ops_any(c->ops);
   c->dOpsG = (double *)c->dalloc(sizeof(double) * sops.size());
@@ -679,7 +1056,7 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   if (cudaMallocHost(&c->hInjected, sizeof(double)) != cudaSuccess) return fail(SWE_ERR_CUDA);
   std::vector<double> wm2(c->Np);
   for (int i = 0; i < c->Np; i++) wm2[i] = 0.5 * c->ops.wmean[i];
-  if (cudaMemcpyAsync(c->dBcaller, B, sizeof(double) * (size_t)c->K * c->Np, cudaMemcpyHostToDevice, c->stream) !=
+  if (cudaMemcpyAsync(c->dBcaller, B, sizeof(double) * (size_t)c->Kin * c->Np, cudaMemcpyHostToDevice, c->stream) !=
           cudaSuccess ||
       cudaMemcpyAsync(c->dWm2, wm2.data(), sizeof(double) * c->Np, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
       cudaMemcpyAsync(c->dOpsG, sops.data(), sizeof(double) * sops.size(), cudaMemcpyHostToDevice, c->stream) !=
@@ -690,6 +1067,15 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
     c->err = "initial upload failed";
     return fail(SWE_ERR_CUDA);
   }
+  if (c->nranks > 1 && c->prm.nccl_id) {
+    ncclUniqueId id;
+    std::memcpy(&id, c->prm.nccl_id, sizeof(id));
+    if (ncclCommInitRank(&c->comm, c->nranks, id, c->rank) != ncclSuccess) {
+      c->err = "ncclCommInitRank failed";
+      c->comm = nullptr;
+      return fail(SWE_ERR_NCCL);
+    }
+  }
   *out = h;
   return SWE_OK;
 }
@@ -697,13 +1083,13 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
 int swe_set_state(swe_ctx *h, const double *hh, const double *hu, const double *hv) {
   if (!h || !hh || !hu || !hv) return SWE_ERR_ARG;
   Ctx *c = &h->c;
-  const size_t KNp = (size_t)c->K * c->Np;
+  const size_t KNp = (size_t)c->Kin * c->Np;
   CK(cudaMemcpyAsync(c->dStage, hh, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dStage + KNp, hu, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dStage + 2 * KNp, hv, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
   double e2 = c->prm.eps_u * c->prm.eps_u, e4 = e2 * e2;
-  k_speeds<<<(c->K + 127) / 128, 128, 0, c->stream>>>(c->K, c->Np, c->g, e4, c->prm.a_floor, c->dStage,
-                                                       c->dStage + KNp, c->dStage + 2 * KNp, c->dAe);
+  k_speeds<<<(c->Kin + 127) / 128, 128, 0, c->stream>>>(c->Kin, c->Np, c->g, e4, c->prm.a_floor, c->dStage,
+                                                         c->dStage + KNp, c->dStage + 2 * KNp, c->dAe);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream));
   CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream));
@@ -718,71 +1104,73 @@ int swe_set_state(swe_ctx *h, const double *hh, const double *hu, const double *
 int swe_step(swe_ctx *h, double dt, int nlevels) {
   if (!h) return SWE_ERR_ARG;
   Ctx *c = &h->c;
-  if (!c->have_state) {
-    c->err = "swe_step before swe_set_state";
+  if (!c->group.empty()) {
+    c->err = "context is linked to an in-process group: use swe_step_group";
     return SWE_ERR_STATE;
   }
-  if (!(dt > 0) || !std::isfinite(dt) || nlevels < 1 || nlevels > 8) {
-    c->err = "invalid dt or nlevels";
-    return SWE_ERR_ARG;
+  std::vector<Ctx *> G = {c};
+  return group_step(G, dt, nlevels);
+}
+
+int swe_link_group(swe_ctx **ctxs, int n) {
+  if (!ctxs || n < 1) return SWE_ERR_ARG;
+  std::vector<Ctx *> G(n, nullptr);
+  for (int i = 0; i < n; i++) {
+    if (!ctxs[i]) return SWE_ERR_ARG;
+    Ctx *c = &ctxs[i]->c;
+    if (c->nranks != n || c->rank < 0 || c->rank >= n || G[c->rank]) return SWE_ERR_ARG;
+    if (c->stream != ctxs[0]->c.stream || c->device != ctxs[0]->c.device) return SWE_ERR_ARG;
+    G[c->rank] = c;
   }
-  if (!c->scheduled) {
-    std::vector<double> ae(c->K);
-    CK(cudaMemcpyAsync(ae.data(), c->dAe, sizeof(double) * c->K, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    c->level.assign(c->K, 1);
-    bin_levels(c->K, c->mesh.hk.data(), ae.data(), nlevels, c->level.data());
-    int rc = materialize(c, c->level, nlevels);
-    if (rc) return rc;
-    c->scheduled = true;
-    c->dt = dt;
-    c->L = nlevels;
-    c->schedule.clear();
-    build_schedule(nlevels, 0, c->schedule);
-  } else if (dt != c->dt || nlevels != c->L) {
-    c->err = "(dt, nlevels) differ from the first swe_step (levels are fixed, P:149)";
-    return SWE_ERR_SCHEDULE;
-  }
-  for (auto &st : c->schedule) {
-    int rc = run_update(c, st.first, c->tick + st.second);
-    if (rc) return rc;
-  }
-  c->tick += 1L << (c->L - 1);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  if (c->prof) collect_profile(c);
-  if (c->hCounters[3] != 0) {
-    c->err = "non-finite values produced";
-    return SWE_ERR_NONFINITE;
-  }
+  for (Ctx *c : G) c->group = G;
   return SWE_OK;
 }
 
-static int ensure_materialized(Ctx *c) {
-  if (c->materialized) return SWE_OK;
-  std::vector<int32_t> ones(c->K, 1);
-  return materialize(c, ones, 1);
+int swe_step_group(swe_ctx **ctxs, int n, double dt, int nlevels) {
+  if (!ctxs || n < 1 || !ctxs[0]) return SWE_ERR_ARG;
+  Ctx *c0 = &ctxs[0]->c;
+  if ((int)c0->group.size() != n) {
+    c0->err = "contexts are not linked (swe_link_group)";
+    return SWE_ERR_STATE;
+  }
+  std::vector<Ctx *> G = c0->group;
+  return group_step(G, dt, nlevels);
 }
 
 int swe_get_state(swe_ctx *h, double *hh, double *hu, double *hv) {
   if (!h || !hh || !hu || !hv) return SWE_ERR_ARG;
   Ctx *c = &h->c;
   if (!c->have_state) return SWE_ERR_STATE;
-  int rc = ensure_materialized(c);
+  std::vector<Ctx *> G = group_of(c);
+  for (Ctx *q : G)
+    if (!q->have_state) return SWE_ERR_STATE;
+  int rc = ensure_materialized_group(G);
   if (rc) return rc;
-  const size_t KNp = (size_t)c->K * c->Np;
-  // gather into the staging buffer's twin: reuse dR slot 2's space is unsafe; use a temporary
+  const size_t KNp = (size_t)c->Kin * c->Np;
   double *tmp = (double *)c->dalloc(sizeof(double) * 3 * KNp);
   if (!tmp) return SWE_ERR_NOMEM;
   GatherParams g = gather_params(c, tmp, tmp + KNp, tmp + 2 * KNp);
-  k_gather_state<<<(c->K + 127) / 128, 128, 0, c->stream>>>(g);
+  k_gather_state<<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaMemcpyAsync(hh, tmp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(hu, tmp + KNp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(hv, tmp + 2 * KNp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (c->kown == c->Kin) {  // every element owned: straight copies
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hh, tmp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hu, tmp + KNp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hv, tmp + 2 * KNp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  } else {  // only owned rows are written
+    std::vector<double> buf(3 * KNp);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(buf.data(), tmp, sizeof(double) * 3 * KNp, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) {
+      double *outs[3] = {hh, hu, hv};
+      for (int k = 0; k < c->kown; k++) {
+        size_t o = (size_t)c->order[k] * c->Np;
+        for (int f = 0; f < 3; f++) std::memcpy(outs[f] + o, &buf[f * KNp + o], sizeof(double) * c->Np);
+      }
+    }
+  }
   c->dfree(tmp);
   if (e != cudaSuccess) return cuda_fail(c, e, "swe_get_state");
   return SWE_OK;
@@ -792,8 +1180,17 @@ void swe_destroy(swe_ctx *h) {
   if (!h) return;
   Ctx *c = &h->c;
   if (c->stream || c->dQ) cudaStreamSynchronize(c->stream);
-  void *ptrs[] = {c->dQ, c->dR, c->dB, c->dV, c->dMeans, c->dUT, c->dTalpha, c->dAe, c->dStage, c->dInjected,
-                  c->dWm2, c->dBcaller, c->dPartials, c->dOpsG, c->dE2E, c->dTcode, c->dOrig, c->dDry, c->dCounters};
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (Ctx *q : c->group)
+    if (q && q != c) {
+      auto &gq = q->group;
+      for (auto &p : gq)
+        if (p == c) p = nullptr;
+    }
+  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha,
+                  c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG,
+                  c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
+                  c->dXrIdx,   c->dDry,   c->dCounters};
   for (void *p : ptrs) c->dfree(p);
   if (c->hCounters) cudaFreeHost(c->hCounters);
   if (c->hInjected) cudaFreeHost(c->hInjected);
@@ -821,7 +1218,7 @@ int swe_get_info(swe_ctx *h, swe_info *info) {
   if (!h || !info) return SWE_ERR_ARG;
   Ctx *c = &h->c;
   std::memset(info, 0, sizeof(*info));
-  info->K = c->K;
+  info->K = c->kown;
   info->Np = c->Np;
   info->N = c->N;
   info->nflipped = c->mesh.nflipped;
@@ -831,9 +1228,10 @@ int swe_get_info(swe_ctx *h, swe_info *info) {
   if (c->scheduled)
     for (int l = 1; l <= c->L; l++) info->level_count[l - 1] = c->off[l] - c->off[l - 1];
   if (!c->have_state) return SWE_OK;
-  int rc = ensure_materialized(c);
+  std::vector<Ctx *> G = group_of(c);
+  int rc = ensure_materialized_group(G);
   if (rc) return rc;
-  int nb = (c->K + 255) / 256;
+  int nb = (c->kown + 255) / 256;
   GatherParams g = gather_params(c, nullptr, nullptr, nullptr);
   k_diag<<<nb, 256, 0, c->stream>>>(g, c->dV, c->dWm2, c->dPartials);
   std::vector<double> part(2 * (size_t)nb);
@@ -877,6 +1275,34 @@ int swe_profile_read(swe_ctx *h, double *times_ms, int64_t *launches, double *by
     if (times_ms) times_ms[i] = c->prof_ms[i];
     if (launches) launches[i] = c->prof_launch[i];
     if (bytes) bytes[i] = c->prof_bytes[i];
+  }
+  return SWE_OK;
+}
+
+int swe_host_halo_plan(const swe_mesh *mesh, const int64_t *gid, const int32_t *owner, int rank, int32_t *counts,
+                       int32_t *peers, int64_t *send_gids, int64_t *recv_gids) {
+  if (!mesh || !owner || !counts) return SWE_ERR_ARG;
+  HostMesh m;
+  std::string err;
+  int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, m, &err);
+  if (rc) return rc;
+  std::vector<int64_t> g(m.K);
+  for (int e = 0; e < m.K; e++) g[e] = gid ? gid[e] : e;
+  HaloPlan plan;
+  build_halo_plan(m, g.data(), owner, rank, plan);
+  int np = (int)plan.peers.size();
+  counts[0] = (int32_t)plan.owned.size();
+  counts[1] = (int32_t)plan.ghosts.size();
+  counts[2] = np;
+  size_t ns = 0, nr = 0;
+  for (int i = 0; i < np; i++) {
+    if (peers) peers[3 * i] = plan.peers[i];
+    if (peers) peers[3 * i + 1] = (int32_t)plan.send[i].size();
+    if (peers) peers[3 * i + 2] = (int32_t)plan.recv[i].size();
+    for (int e : plan.send[i])
+      if (send_gids) send_gids[ns++] = g[e];
+    for (int e : plan.recv[i])
+      if (recv_gids) recv_gids[nr++] = g[e];
   }
   return SWE_OK;
 }

@@ -252,7 +252,8 @@ def c4_dambreak(N: int = 3, base: int = 1, shuffle_seed: int | None = SEED) -> W
 C5_LX = 2.0e6
 
 
-def c5_tsunami(P: int = 1, base_n: int = 1280, strip: int = 1, shuffle_seed: int | None = SEED) -> Workload:
+def c5_tsunami(P: int = 1, base_n: int = 1280, strip: int = 1, shuffle_seed: int | None = SEED,
+               rows: tuple | None = None) -> Workload:
     """C5: synthetic ocean-basin tsunami, N=3, 4 MRAB levels.
 
     Domain [0, 2000 km] x [0, W], W = 2000 km * P / strip.  Base spacing 2000 km / base_n
@@ -260,8 +261,9 @@ def c5_tsunami(P: int = 1, base_n: int = 1280, strip: int = 1, shuffle_seed: int
     2 bisections for d < 400 km, 4 for d < 60 km, 6 for d < 8 km.  strip > 1 keeps a 1/strip
     y-strip of the same mesh (bounded CPU-oracle sample)."""
     ny = base_n * P // strip
-    W = C5_LX / base_n * ny
-    m = nvb_graded(base_n, ny, 0.0, C5_LX, 0.0, W,
+    hb = C5_LX / base_n
+    j0, j1 = (0, ny) if rows is None else (max(0, rows[0]), min(ny, rows[1]))
+    m = nvb_graded(base_n, j1 - j0, 0.0, C5_LX, j0 * hb, j1 * hb,
                    [(C5_LX - 400e3, C5_LX + 1, 2), (C5_LX - 60e3, C5_LX + 1, 4), (C5_LX - 8e3, C5_LX + 1, 6)])
     if shuffle_seed is not None:
         m = shuffle(m, shuffle_seed)
@@ -281,3 +283,24 @@ def c5_tsunami(P: int = 1, base_n: int = 1280, strip: int = 1, shuffle_seed: int
     # a_floor = 200 m/s >= sqrt(g * 4001 m): levels are purely geometric (reading A19/C5)
     prm = dict(h0=1e-3, tvb_M=1e-3, tvb_nu=1.5, a_floor=200.0, use_pp=1, use_tvb=1)
     return Workload(f"C5-P{P}" + (f"-strip{strip}" if strip > 1 else ""), m, 3, 9.81, B, init, prm, 4, 0.2, 20)
+
+
+def centroid_keys(mesh: Mesh, h: float) -> np.ndarray:
+    """Global element ids from exact centroid keys (dyadic vertex coordinates: 3*centroid is a
+    multiple of h/64 for up to 6 NVB bisections of an h-spaced base grid)."""
+    v = mesh.etov
+    ix = np.round(mesh.vx[v].sum(1) * 64.0 / h).astype(np.int64)
+    iy = np.round(mesh.vy[v].sum(1) * 64.0 / h).astype(np.int64)
+    return (ix << 32) | iy
+
+
+def c5_rank_strip(rank: int, nranks: int, base_n: int = 1280):
+    """Rank `rank`'s share of the weak-scaling C5 basin ([0, 2000 km] x [0, 2000 km * nranks]):
+    its own 2000 km y-strip plus two buffer rows on each side (ghost layer + refinement buffer);
+    owner by centroid y, gid by exact centroid key."""
+    hb = C5_LX / base_n
+    w = c5_tsunami(P=nranks, base_n=base_n, rows=(rank * base_n - 2, (rank + 1) * base_n + 2), shuffle_seed=None)
+    v = w.mesh.etov
+    cy = w.mesh.vy[v].mean(1)
+    owner = np.clip(np.floor(cy / C5_LX).astype(np.int32), 0, nranks - 1)
+    return w, owner, centroid_keys(w.mesh, hb)
