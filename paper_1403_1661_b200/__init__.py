@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libswe_b200.so")
+LIB_PATH = os.environ.get("SWE_LIB", os.path.join(_HERE, "libswe_b200.so"))  # SWE_LIB: A/B variants
 
 SWE_ERRORS = {0: "SWE_OK", -1: "SWE_ERR_ARG", -2: "SWE_ERR_MESH", -3: "SWE_ERR_ORDER", -4: "SWE_ERR_STATE",
               -5: "SWE_ERR_SCHEDULE", -6: "SWE_ERR_NONFINITE", -7: "SWE_ERR_CUDA", -8: "SWE_ERR_NCCL",

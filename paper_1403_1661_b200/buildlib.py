@@ -36,7 +36,12 @@ def _stale(out: str, inputs: list[str]) -> bool:
     return any(os.path.getmtime(i) > t for i in inputs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: str | None = None) -> str:
+    """defines/out: build an A/B variant (e.g. ("VOL_UNROLL=2",), "libswe_u2.so") next to the main library."""
+    global BUILD, LIB
+    if defines or out:
+        tag = "_".join(d.replace("=", "") for d in defines) or "variant"
+        BUILD, LIB = os.path.join(HERE, "_build_" + tag), os.path.join(HERE, out or f"libswe_{tag}.so")
     os.makedirs(BUILD, exist_ok=True)
     hdr = os.path.join(ROOT, "include", "swe.h")
     deps = [os.path.join(CSRC, d) for d in DEPS] + [hdr, __file__]
@@ -52,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")
         if force or _stale(obj, [src] + deps):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-I", _nccl_dirs()[0], "-Xcompiler", "-fPIC,-ffp-contract=off",
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *[f"-D{d}" for d in defines], "-I", _nccl_dirs()[0],
+                   "-Xcompiler", "-fPIC,-ffp-contract=off",
                    "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
             subprocess.check_call(cmd)
         objs.append(obj)
@@ -66,5 +72,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs))

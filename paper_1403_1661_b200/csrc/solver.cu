@@ -204,6 +204,13 @@ struct Ctx {
   }
 };
 
+// sum of one counter over its kSlots (host copy)
+static unsigned long long counter(const Ctx *c, int which) {
+  unsigned long long s = 0;
+  for (int i = 0; i < kSlots; i++) s += c->hCounters[which * kSlots + i];
+  return s;
+}
+
 static int cuda_fail(Ctx *c, cudaError_t e, const char *where) {
   c->err = std::string(where) + ": " + cudaGetErrorString(e);
   return SWE_ERR_CUDA;
@@ -622,8 +629,8 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
                                              c->dQ);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
-  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream));
-  CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream));
+  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
+  CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream));
   c->n_updates = 0;
   for (int l = 0; l <= 8; l++) {
     c->kcount[l] = 0;
@@ -878,14 +885,14 @@ static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
     {
       Ctx *c = c_;
       CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost,
+      CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 4 * kSlots, cudaMemcpyDeviceToHost,
                          c->stream));
     }
   }
   for (Ctx *c : G) {
     CK(cudaStreamSynchronize(c->stream));
     if (c->prof) collect_profile(c);
-    if (c->hCounters[3] != 0) {
+    if (counter(c, 3) != 0) {
       c->err = "non-finite values produced";
       return SWE_ERR_NONFINITE;
     }
@@ -1049,11 +1056,11 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   c->dWm2 = (double *)c->dalloc(sizeof(double) * c->Np);
   std::vector<double> sops = smem_ops_any(c->ops);
   c->dOpsG = (double *)c->dalloc(sizeof(double) * sops.size());
-  c->dCounters = (unsigned long long *)c->dalloc(sizeof(unsigned long long) * 8);
-  c->dInjected = (double *)c->dalloc(sizeof(double));
+  c->dCounters = (unsigned long long *)c->dalloc(sizeof(unsigned long long) * 4 * kSlots);
+  c->dInjected = (double *)c->dalloc(sizeof(double) * kSlots);
   if (!c->alloc_ok) return fail(SWE_ERR_NOMEM);
-  if (cudaMallocHost(&c->hCounters, sizeof(unsigned long long) * 8) != cudaSuccess) return fail(SWE_ERR_CUDA);
-  if (cudaMallocHost(&c->hInjected, sizeof(double)) != cudaSuccess) return fail(SWE_ERR_CUDA);
+  if (cudaMallocHost(&c->hCounters, sizeof(unsigned long long) * 4 * kSlots) != cudaSuccess) return fail(SWE_ERR_CUDA);
+  if (cudaMallocHost(&c->hInjected, sizeof(double) * kSlots) != cudaSuccess) return fail(SWE_ERR_CUDA);
   std::vector<double> wm2(c->Np);
   for (int i = 0; i < c->Np; i++) wm2[i] = 0.5 * c->ops.wmean[i];
   if (cudaMemcpyAsync(c->dBcaller, B, sizeof(double) * (size_t)c->Kin * c->Np, cudaMemcpyHostToDevice, c->stream) !=
@@ -1061,8 +1068,8 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
       cudaMemcpyAsync(c->dWm2, wm2.data(), sizeof(double) * c->Np, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
       cudaMemcpyAsync(c->dOpsG, sops.data(), sizeof(double) * sops.size(), cudaMemcpyHostToDevice, c->stream) !=
           cudaSuccess ||
-      cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream) != cudaSuccess ||
       cudaStreamSynchronize(c->stream) != cudaSuccess) {
     c->err = "initial upload failed";
     return fail(SWE_ERR_CUDA);
@@ -1091,8 +1098,8 @@ int swe_set_state(swe_ctx *h, const double *hh, const double *hu, const double *
   k_speeds<<<(c->Kin + 127) / 128, 128, 0, c->stream>>>(c->Kin, c->Np, c->g, e4, c->prm.a_floor, c->dStage,
                                                          c->dStage + KNp, c->dStage + 2 * KNp, c->dAe);
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 8, c->stream));
-  CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double), c->stream));
+  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
+  CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream));
   c->have_state = true;
   c->materialized = false;
   c->scheduled = false;
@@ -1237,8 +1244,8 @@ int swe_get_info(swe_ctx *h, swe_info *info) {
   std::vector<double> part(2 * (size_t)nb);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(part.data(), c->dPartials, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->hInjected, c->dInjected, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 4 * kSlots, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hInjected, c->dInjected, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   double mass = 0.0, mn = 1e300;
   for (int b = 0; b < nb; b++) {
@@ -1247,10 +1254,12 @@ int swe_get_info(swe_ctx *h, swe_info *info) {
   }
   info->mass = mass;
   info->min_h = mn;
-  info->injected_mass = *c->hInjected;
-  info->n_pp = (int64_t)c->hCounters[0];
-  info->n_dry = (int64_t)c->hCounters[1];
-  info->n_tvb = (int64_t)c->hCounters[2];
+  double inj = 0.0;
+  for (int i = 0; i < kSlots; i++) inj += c->hInjected[i];
+  info->injected_mass = inj;
+  info->n_pp = (int64_t)counter(c, 0);
+  info->n_dry = (int64_t)counter(c, 1);
+  info->n_tvb = (int64_t)counter(c, 2);
   return SWE_OK;
 }
 
