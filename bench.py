@@ -266,9 +266,13 @@ def main():
             "k1_share_of_step": prof["k1_ms"] / ms if ms > 0 else None,
             "k2_share_of_step": prof["k2_ms"] / ms if ms > 0 else None}
     traffic_path = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
-    if os.path.exists(traffic_path):
+    if os.path.exists(traffic_path):  # one ncu --set full capture (profiles/), not measured in this run
         try:
-            roof["traffic"] = json.load(open(traffic_path)).get("bytes_per_launch_per_elem_update")
+            tr = json.load(open(traffic_path))
+            roof["traffic"] = tr["bytes_per_launch"]
+            roof["traffic_launch_elements"] = tr["elements"]
+            roof["traffic_bytes_per_elem_update"] = tr["bytes_per_elem_update"]
+            roof["algorithmic_bytes_per_elem_update"] = tr["algorithmic_bytes_per_elem_update"]
         except Exception:
             pass
 
