@@ -4,8 +4,8 @@
 // Blend interpolation nodes ... cubature rules for triangles ... Gauss
 // quadrature rules"), P:651 (P, Pr, Ps "projection matrices that are pre
 // multiplied with cubature integration weights"), P:691 (lift L^g).
-// Readings: SURVEY §8(c) O1-O3, A2 (collapsed Gauss-Jacobi cubature of strength
-// 2N+1, Ng = N+1 Gauss points per edge), A8 (HW alpha table).
+// Readings: SURVEY §8(c) O1-O3, A2' (symmetric degree-2N cubature for N <= 5,
+// collapsed Gauss-Jacobi above; Ng = N+1 Gauss points per edge), A8 (HW alpha table).
 //
 // Everything here is computed in long double (x87 80-bit) and rounded to
 // double once at the end: the tensor-Legendre basis L_p(r)L_q(s) is
@@ -340,13 +340,173 @@ Mat interp_matrix(const RefElement &re, const std::vector<double> &r, const std:
   return to_double(t_matmul(vandermonde(re.N, R, S, 0), Vinv));
 }
 
+// ---------------------------------------------------------------- cubature
+// P:81 "The volume integrals are computed using cubature rules for triangles
+// [Cools]"; P:108-110 (Fig. 1): polynomial order 5 with "integration order 10",
+// i.e. a symmetric rule of degree 2N.  Reading A2': for N <= 5 the
+// fully symmetric rules of Dunavant (1985, IJNME 21:1129, Tables; also listed
+// in Cools' encyclopedia) -- 3, 6, 12, 16, 25 points for degrees 2, 4, 6, 8, 10.
+// The tabulated 15-digit values are only the starting point: the rule is the
+// root of its moment equations, refined here in long double by Gauss-Newton on
+// "sum_i w_i r_i^a s_i^b = int_T r^a s^b for all a+b <= 2N".
+// Orbits (barycentric (l1,l2,l3) -> (r,s) = l1 v0 + l2 v1 + l3 v2):
+//   S3  : centroid;
+//   S21 : (a,b,b),(b,a,b),(b,b,a) with b = (1-a)/2;
+//   S111: (a,b,c),(b,c,a),(c,a,b),(b,a,c),(c,b,a),(a,c,b) with c = 1-a-b.
+// Points are listed orbit by orbit in table order, weights scaled to area 2.
+struct Orbit {
+  int type;           // 1 = S3, 3 = S21, 6 = S111
+  LD w, a, b;         // weight (sum over all points = 1 in the table) and coordinates
+};
+
+static std::vector<Orbit> dunavant_table(int N) {
+  switch (N) {
+    case 1: return {{3, 1.0L / 3.0L, 2.0L / 3.0L, 0}};
+    case 2: return {{3, 0.223381589678011L, 0.108103018168070L, 0},
+                    {3, 0.109951743655322L, 0.816847572980459L, 0}};
+    case 3: return {{3, 0.116786275726379L, 0.501426509658179L, 0},
+                    {3, 0.050844906370207L, 0.873821971016996L, 0},
+                    {6, 0.082851075618374L, 0.053145049844817L, 0.310352451033784L}};
+    case 4: return {{1, 0.144315607677787L, 0, 0},
+                    {3, 0.095091634267285L, 0.081414823414554L, 0},
+                    {3, 0.103217370534718L, 0.658861384496480L, 0},
+                    {3, 0.032458497623198L, 0.898905543365938L, 0},
+                    {6, 0.027230314174435L, 0.008394777409958L, 0.263112829634638L}};
+    case 5: return {{1, 0.090817990382754L, 0, 0},
+                    {3, 0.036725957756467L, 0.028844733232685L, 0},
+                    {3, 0.045321059435528L, 0.781036849029926L, 0},
+                    {6, 0.072757916845420L, 0.141707219414880L, 0.307939838764121L},
+                    {6, 0.028327242531057L, 0.025003534762686L, 0.246672560639903L},
+                    {6, 0.009421666963733L, 0.009540815400299L, 0.066803251012200L}};
+    default: return {};
+  }
+}
+
+static void orbit_points(const std::vector<Orbit> &orb, std::vector<LD> &r, std::vector<LD> &s, std::vector<LD> &w) {
+  r.clear();
+  s.clear();
+  w.clear();
+  auto push = [&](LD l1, LD l2, LD l3, LD wt) {
+    r.push_back(-l1 + l2 - l3);
+    s.push_back(-l1 - l2 + l3);
+    w.push_back(2 * wt);
+  };
+  for (const Orbit &o : orb) {
+    if (o.type == 1) {
+      push(1.0L / 3, 1.0L / 3, 1.0L / 3, o.w);
+    } else if (o.type == 3) {
+      LD a = o.a, b = (1 - o.a) / 2;
+      push(a, b, b, o.w);
+      push(b, a, b, o.w);
+      push(b, b, a, o.w);
+    } else {
+      LD a = o.a, b = o.b, c = 1 - o.a - o.b;
+      push(a, b, c, o.w);
+      push(b, c, a, o.w);
+      push(c, a, b, o.w);
+      push(b, a, c, o.w);
+      push(c, b, a, o.w);
+      push(a, c, b, o.w);
+    }
+  }
+}
+
+// int_T r^a s^b over T = {r,s >= -1, r+s <= 0}: with r = 2x-1, s = 2y-1 on the
+// unit simplex, int x^i y^j = i! j! / (i+j+2)!.
+static LD tri_monomial(int a, int b) {
+  auto fact = [](int n) { LD f = 1; for (int k = 2; k <= n; k++) f *= k; return f; };
+  auto binom = [&](int n, int k) { return fact(n) / (fact(k) * fact(n - k)); };
+  LD acc = 0;
+  for (int i = 0; i <= a; i++)
+    for (int j = 0; j <= b; j++) {
+      LD sign = ((a - i + b - j) % 2) ? -1 : 1;
+      acc += sign * binom(a, i) * binom(b, j) * std::pow(2.0L, i + j) * fact(i) * fact(j) / fact(i + j + 2);
+    }
+  return 4 * acc;
+}
+
+static bool ld_symmetric_rule(int N, std::vector<LD> &rc, std::vector<LD> &sc, std::vector<LD> &wc) {
+  std::vector<Orbit> orb = dunavant_table(N);
+  if (orb.empty()) return false;
+  const int deg = 2 * N;
+  // unknown vector theta: per orbit w, then a (S21, S111), then b (S111)
+  auto pack = [&](const std::vector<Orbit> &o) {
+    std::vector<LD> t;
+    for (const Orbit &x : o) {
+      t.push_back(x.w);
+      if (x.type >= 3) t.push_back(x.a);
+      if (x.type == 6) t.push_back(x.b);
+    }
+    return t;
+  };
+  auto unpack = [&](const std::vector<LD> &t) {
+    std::vector<Orbit> o = orb;
+    size_t k = 0;
+    for (Orbit &x : o) {
+      x.w = t[k++];
+      if (x.type >= 3) x.a = t[k++];
+      if (x.type == 6) x.b = t[k++];
+    }
+    return o;
+  };
+  std::vector<std::pair<int, int>> mono;
+  std::vector<LD> exact;
+  for (int a = 0; a <= deg; a++)
+    for (int b = 0; a + b <= deg; b++) {
+      mono.push_back({a, b});
+      exact.push_back(tri_monomial(a, b));
+    }
+  auto residual = [&](const std::vector<LD> &t) {
+    std::vector<LD> r, s, w, res(mono.size());
+    orbit_points(unpack(t), r, s, w);
+    for (size_t m = 0; m < mono.size(); m++) {
+      LD acc = 0;
+      for (size_t i = 0; i < w.size(); i++)
+        acc += w[i] * std::pow(r[i], (LD)mono[m].first) * std::pow(s[i], (LD)mono[m].second);
+      res[m] = acc - exact[m];
+    }
+    return res;
+  };
+  std::vector<LD> theta = pack(orb);
+  const int n = (int)theta.size(), m = (int)mono.size();
+  for (int it = 0; it < 12; it++) {
+    std::vector<LD> r0 = residual(theta);
+    LMat J(m, n);
+    for (int j = 0; j < n; j++) {  // central differences in long double
+      const LD h = 1e-7L;
+      std::vector<LD> tp = theta, tm = theta;
+      tp[j] += h;
+      tm[j] -= h;
+      std::vector<LD> rp = residual(tp), rm = residual(tm);
+      for (int i = 0; i < m; i++) J(i, j) = (rp[i] - rm[i]) / (2 * h);
+    }
+    LMat JtJ(n, n), Jtr(n, 1);
+    for (int a = 0; a < n; a++) {
+      for (int b = 0; b < n; b++) {
+        LD acc = 0;
+        for (int i = 0; i < m; i++) acc += J(i, a) * J(i, b);
+        JtJ(a, b) = acc;
+      }
+      LD acc = 0;
+      for (int i = 0; i < m; i++) acc += J(i, a) * r0[i];
+      Jtr(a, 0) = acc;
+    }
+    LMat d = t_matmul(t_inverse(JtJ), Jtr);
+    for (int j = 0; j < n; j++) theta[j] -= d(j, 0);
+  }
+  LD worst = 0;
+  for (LD v : residual(theta)) worst = std::max(worst, std::fabs(v));
+  if (!(worst < 1e-16L)) throw std::runtime_error("symmetric cubature: Newton did not converge");
+  orbit_points(unpack(theta), rc, sc, wc);
+  return true;
+}
+
 void build_refel(int N, RefElement &re) {
   re.N = N;
   re.Np = (N + 1) * (N + 2) / 2;
   re.Nfp = N + 1;
   re.Ng = N + 1;
   int q = N + 1, Np = re.Np;
-  re.Ncub = q * q;
   std::vector<LD> r, s;
   ld_nodes(N, r, s);
   re.r = to_double(r);
@@ -361,17 +521,23 @@ void build_refel(int N, RefElement &re) {
   re.Dr = to_double(Dr);
   re.Ds = to_double(Ds);
 
-  // Collapsed (Stroud) cubature: r = (1+a)(1-b)/2 - 1, s = b, dr ds = (1-b)/2 da db;
-  // Gauss-Legendre in a, Gauss-Jacobi(1,0) in b: exact to degree 2q-1 = 2N+1.
-  std::vector<LD> xa, wa, xb, wb, rc, sc, wc;
-  ld_gauss_legendre(q, xa, wa);
-  ld_gauss_jacobi10(q, xb, wb);
-  for (int j = 0; j < q; j++)
-    for (int i = 0; i < q; i++) {
-      rc.push_back(0.5L * (1 + xa[i]) * (1 - xb[j]) - 1);
-      sc.push_back(xb[j]);
-      wc.push_back(0.5L * wa[i] * wb[j]);
-    }
+  // Volume cubature (reading A2'): the symmetric degree-2N rule for N <= 5;
+  // above that (no tabulated rule here) the collapsed (Stroud) rule
+  // r = (1+a)(1-b)/2 - 1, s = b, dr ds = (1-b)/2 da db, Gauss-Legendre in a,
+  // Gauss-Jacobi(1,0) in b, exact to degree 2q-1 = 2N+1.
+  std::vector<LD> rc, sc, wc;
+  if (!ld_symmetric_rule(N, rc, sc, wc)) {
+    std::vector<LD> xa, wa, xb, wb;
+    ld_gauss_legendre(q, xa, wa);
+    ld_gauss_jacobi10(q, xb, wb);
+    for (int j = 0; j < q; j++)
+      for (int i = 0; i < q; i++) {
+        rc.push_back(0.5L * (1 + xa[i]) * (1 - xb[j]) - 1);
+        sc.push_back(xb[j]);
+        wc.push_back(0.5L * wa[i] * wb[j]);
+      }
+  }
+  re.Ncub = (int)wc.size();
   re.rc = to_double(rc);
   re.sc = to_double(sc);
   re.wc = to_double(wc);
@@ -398,7 +564,7 @@ void build_refel(int N, RefElement &re) {
   re.Ic = to_double(Ic);
   re.Ig = to_double(Ig);
 
-  // Mref_ij = int l_i l_j = sum_c w_c Ic_ci Ic_cj (exact: degree 2N <= 2N+1)
+  // Mref_ij = int l_i l_j = sum_c w_c Ic_ci Ic_cj (exact: degree 2N <= the rule's strength)
   LMat Mref(Np, Np);
   for (int i = 0; i < Np; i++)
     for (int j = 0; j < Np; j++) {

@@ -597,7 +597,9 @@ int orc_refel_sizes(int N, int *out) {
   if (N < 1 || N > 8) return -3;
   out[0] = (N + 1) * (N + 2) / 2;
   out[1] = N + 1;
-  out[2] = (N + 1) * (N + 1);
+  RefElement re;
+  build_refel(N, re);
+  out[2] = re.Ncub;
   out[3] = N + 1;
   return 0;
 }

@@ -7,9 +7,9 @@
 //   psi_ij(r,s) = sqrt2 Phat_i^{(0,0)}(a) Phat_j^{(2i+1,0)}(b) (1-b)^i,
 //   a = 2(1+r)/(1-s) - 1, b = s,
 // and Gauss rules obtained as eigenvalues of the Jacobi matrix (Sturm
-// bisection, Golub-Welsch weights).  Readings: cubature =
-// collapsed Gauss-Jacobi with q = N+1 points per direction (strength 2N+1
-// >= the paper's 2N); Ng = N+1 Gauss points per face.
+// bisection, Golub-Welsch weights).  Readings: cubature = the
+// symmetric degree-2N rule (A2', the paper's "integration order 2N" from
+// Cools' rules) for N <= 5; Ng = N+1 Gauss points per face.
 #include <algorithm>
 #include <cmath>
 
@@ -271,6 +271,146 @@ void nodes2d(int N, std::vector<double> &r, std::vector<double> &s) {
   }
 }
 
+// Symmetric degree-2N triangle cubature ("cubature rules for triangles",
+// P:108-110 "integration order 10" at N = 5; reading A2').  Orbit structure and
+// 15-digit starting values from Dunavant (1985), Tables for degrees 2-10;
+// the rule is the Newton root of the orthonormal moment equations
+//   sum_i w_i psi_k(r_i, s_i) = int_T psi_k = sqrt(2) delta_k0,  deg psi_k <= 2N,
+// with the analytic Jacobian through the Dubiner gradients.  Point order:
+// orbits in table order; a point is a permutation of the orbit's barycentric
+// triple t = (a, b, c) (S21: b = c = (1-a)/2; S111: c = 1-a-b), barycentric
+// l_k = t[perm[k]], (r, s) = l0 (-1,-1) + l1 (1,-1) + l2 (-1,1).
+struct SymOrbit {
+  int npts;  // 1, 3 or 6
+  double w, a, b;
+};
+
+bool dunavant_start(int N, std::vector<SymOrbit> &orb) {
+  static const SymOrbit d2[] = {{3, 1.0 / 3.0, 2.0 / 3.0, 0.0}};
+  static const SymOrbit d4[] = {{3, 0.223381589678011, 0.108103018168070, 0.0},
+                                {3, 0.109951743655322, 0.816847572980459, 0.0}};
+  static const SymOrbit d6[] = {{3, 0.116786275726379, 0.501426509658179, 0.0},
+                                {3, 0.050844906370207, 0.873821971016996, 0.0},
+                                {6, 0.082851075618374, 0.053145049844817, 0.310352451033784}};
+  static const SymOrbit d8[] = {{1, 0.144315607677787, 0.0, 0.0},
+                                {3, 0.095091634267285, 0.081414823414554, 0.0},
+                                {3, 0.103217370534718, 0.658861384496480, 0.0},
+                                {3, 0.032458497623198, 0.898905543365938, 0.0},
+                                {6, 0.027230314174435, 0.008394777409958, 0.263112829634638}};
+  static const SymOrbit d10[] = {{1, 0.090817990382754, 0.0, 0.0},
+                                 {3, 0.036725957756467, 0.028844733232685, 0.0},
+                                 {3, 0.045321059435528, 0.781036849029926, 0.0},
+                                 {6, 0.072757916845420, 0.141707219414880, 0.307939838764121},
+                                 {6, 0.028327242531057, 0.025003534762686, 0.246672560639903},
+                                 {6, 0.009421666963733, 0.009540815400299, 0.066803251012200}};
+  const SymOrbit *t = nullptr;
+  size_t n = 0;
+  switch (N) {
+    case 1: t = d2, n = 1; break;
+    case 2: t = d4, n = 2; break;
+    case 3: t = d6, n = 3; break;
+    case 4: t = d8, n = 5; break;
+    case 5: t = d10, n = 6; break;
+    default: return false;
+  }
+  orb.assign(t, t + n);
+  return true;
+}
+
+// perm tables: barycentric slot k takes orbit coordinate perm[k] (0 = a, 1 = b, 2 = c)
+const int kPerm3[3][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}};
+const int kPerm6[6][3] = {{0, 1, 2}, {1, 2, 0}, {2, 0, 1}, {1, 0, 2}, {2, 1, 0}, {0, 2, 1}};
+
+// Points, weights and d(r,s)/d(a,b) of every point of the orbits.
+void expand_orbits(const std::vector<SymOrbit> &orb, std::vector<double> &r, std::vector<double> &s,
+                   std::vector<double> &w, std::vector<double> &drda, std::vector<double> &dsda,
+                   std::vector<double> &drdb, std::vector<double> &dsdb) {
+  r.clear(), s.clear(), w.clear(), drda.clear(), dsda.clear(), drdb.clear(), dsdb.clear();
+  const double vr[3] = {-1.0, 1.0, -1.0}, vs[3] = {-1.0, -1.0, 1.0};
+  for (const SymOrbit &o : orb) {
+    for (int p = 0; p < o.npts; p++) {
+      double l[3], la[3], lb[3];
+      for (int k = 0; k < 3; k++) {
+        int c = o.npts == 1 ? -1 : (o.npts == 3 ? kPerm3[p][k] : kPerm6[p][k]);
+        if (c < 0) {
+          l[k] = 1.0 / 3.0, la[k] = 0.0, lb[k] = 0.0;
+        } else if (o.npts == 3) {
+          l[k] = c == 0 ? o.a : 0.5 * (1.0 - o.a);
+          la[k] = c == 0 ? 1.0 : -0.5;
+          lb[k] = 0.0;
+        } else {
+          l[k] = c == 0 ? o.a : (c == 1 ? o.b : 1.0 - o.a - o.b);
+          la[k] = c == 0 ? 1.0 : (c == 1 ? 0.0 : -1.0);
+          lb[k] = c == 1 ? 1.0 : (c == 0 ? 0.0 : -1.0);
+        }
+      }
+      double rr = 0, ss = 0, ra = 0, sa = 0, rb = 0, sb = 0;
+      for (int k = 0; k < 3; k++) {
+        rr += l[k] * vr[k], ss += l[k] * vs[k];
+        ra += la[k] * vr[k], sa += la[k] * vs[k];
+        rb += lb[k] * vr[k], sb += lb[k] * vs[k];
+      }
+      r.push_back(rr), s.push_back(ss), w.push_back(2.0 * o.w);
+      drda.push_back(ra), dsda.push_back(sa), drdb.push_back(rb), dsdb.push_back(sb);
+    }
+  }
+}
+
+bool symmetric_cubature(int N, std::vector<double> &rc, std::vector<double> &sc, std::vector<double> &wc) {
+  std::vector<SymOrbit> orb;
+  if (!dunavant_start(N, orb)) return false;
+  const int deg = 2 * N, nmom = (deg + 1) * (deg + 2) / 2;
+  int nunk = 0;
+  for (const SymOrbit &o : orb) nunk += o.npts == 1 ? 1 : (o.npts == 3 ? 2 : 3);
+  std::vector<double> r, s, w, ra, sa, rb, sb;
+  for (int it = 0; it < 8; it++) {
+    expand_orbits(orb, r, s, w, ra, sa, rb, sb);
+    const int np = (int)w.size();
+    DMat F = vandermonde(deg, r, s, 0), Fr = vandermonde(deg, r, s, 1), Fs = vandermonde(deg, r, s, 2);
+    DMat J(nmom, nunk);
+    std::vector<double> res(nmom, 0.0);
+    for (int k = 0; k < nmom; k++) res[k] = k == 0 ? -std::sqrt(2.0) : 0.0;
+    int p0 = 0, u = 0;
+    for (const SymOrbit &o : orb) {
+      for (int p = p0; p < p0 + o.npts; p++)
+        for (int k = 0; k < nmom; k++) {
+          res[k] += w[p] * F(p, k);
+          J(k, u) += 2.0 * F(p, k);  // d/d(table weight); point weight = 2 w
+          if (o.npts >= 3) J(k, u + 1) += w[p] * (Fr(p, k) * ra[p] + Fs(p, k) * sa[p]);
+          if (o.npts == 6) J(k, u + 2) += w[p] * (Fr(p, k) * rb[p] + Fs(p, k) * sb[p]);
+        }
+      p0 += o.npts;
+      u += o.npts == 1 ? 1 : (o.npts == 3 ? 2 : 3);
+    }
+    (void)np;
+    // least-squares step: (J^T J) d = J^T res
+    DMat Jt = transpose(J), JtJ = mul(Jt, J), JtJinv;
+    if (!invert(JtJ, JtJinv)) return false;
+    std::vector<double> g(nunk, 0.0), d(nunk, 0.0);
+    for (int i = 0; i < nunk; i++)
+      for (int k = 0; k < nmom; k++) g[i] += Jt(i, k) * res[k];
+    for (int i = 0; i < nunk; i++)
+      for (int j = 0; j < nunk; j++) d[i] += JtJinv(i, j) * g[j];
+    u = 0;
+    for (SymOrbit &o : orb) {
+      o.w -= d[u++];
+      if (o.npts >= 3) o.a -= d[u++];
+      if (o.npts == 6) o.b -= d[u++];
+    }
+  }
+  expand_orbits(orb, r, s, w, ra, sa, rb, sb);
+  DMat F = vandermonde(deg, r, s, 0);
+  double worst = 0.0;
+  for (int k = 0; k < nmom; k++) {
+    double acc = k == 0 ? -std::sqrt(2.0) : 0.0;
+    for (size_t p = 0; p < w.size(); p++) acc += w[p] * F((int)p, k);
+    worst = std::max(worst, std::fabs(acc));
+  }
+  if (!(worst < 1e-14)) return false;
+  rc = r, sc = s, wc = w;
+  return true;
+}
+
 }  // namespace
 
 bool build_refops(int N, RefOps &o, std::string *err) {
@@ -283,7 +423,6 @@ bool build_refops(int N, RefOps &o, std::string *err) {
   o.Nfp = N + 1;
   o.Ng = N + 1;
   const int q = N + 1, Np = o.Np;
-  o.Nc = q * q;
   nodes2d(N, o.r, o.s);
   o.V = vandermonde(N, o.r, o.s, 0);
   if (!invert(o.V, o.Vinv)) {
@@ -295,19 +434,28 @@ bool build_refops(int N, RefOps &o, std::string *err) {
   DMat MrefInv = mul(o.V, transpose(o.V));  // (V V^T) = Mref^{-1} for an orthonormal basis
   invert(MrefInv, o.Mref);
 
-  // cubature: Gauss-Legendre (a) x Gauss-Jacobi(1,0) (b), r = (1+a)(1-b)/2 - 1, s = b
-  std::vector<double> xa, wa, xb, wb;
-  gauss_rule(q, 0.0, 0.0, xa, wa);
-  gauss_rule(q, 1.0, 0.0, xb, wb);
+  // cubature (A2'): symmetric degree 2N for N <= 5, else collapsed
+  // Gauss-Legendre (a) x Gauss-Jacobi(1,0) (b), r = (1+a)(1-b)/2 - 1, s = b
   o.rc.clear();
   o.sc.clear();
   o.wc.clear();
-  for (int jb = 0; jb < q; jb++)
-    for (int ia = 0; ia < q; ia++) {
-      o.rc.push_back(0.5 * (1.0 + xa[ia]) * (1.0 - xb[jb]) - 1.0);
-      o.sc.push_back(xb[jb]);
-      o.wc.push_back(0.5 * wa[ia] * wb[jb]);
+  if (N <= 5) {
+    if (!symmetric_cubature(N, o.rc, o.sc, o.wc)) {
+      if (err) *err = "symmetric cubature did not converge";
+      return false;
     }
+  } else {
+    std::vector<double> xa, wa, xb, wb;
+    gauss_rule(q, 0.0, 0.0, xa, wa);
+    gauss_rule(q, 1.0, 0.0, xb, wb);
+    for (int jb = 0; jb < q; jb++)
+      for (int ia = 0; ia < q; ia++) {
+        o.rc.push_back(0.5 * (1.0 + xa[ia]) * (1.0 - xb[jb]) - 1.0);
+        o.sc.push_back(xb[jb]);
+        o.wc.push_back(0.5 * wa[ia] * wb[jb]);
+      }
+  }
+  o.Nc = (int)o.wc.size();
   gauss_rule(o.Ng, 0.0, 0.0, o.tg, o.wg);
 
   std::vector<double> rg, sg;

@@ -54,6 +54,31 @@ __global__ void k_scatter_state(int K, int Np, const int *orig, const double *h,
   }
 }
 
+// Static TVB geometry of every element (P:224-253 limiter stencil): Hk = 4A / perimeter
+// (level-binning geometry) and the unit vectors from the centroid to the three edge midpoints,
+// with the exact expressions K2 used when it derived them per launch.
+__global__ void k_tvb_geo(int K, const double *V, double *tgeo) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= K) return;
+  const double XV[3] = {V[e], V[K + e], V[2 * (size_t)K + e]};
+  const double YV[3] = {V[3 * (size_t)K + e], V[4 * (size_t)K + e], V[5 * (size_t)K + e]};
+  const double A = 0.5 * ((XV[1] - XV[0]) * (YV[2] - YV[0]) - (XV[2] - XV[0]) * (YV[1] - YV[0]));
+  double len[3];
+  for (int f = 0; f < 3; f++) {
+    const double dx = XV[(f + 1) % 3] - XV[f], dy = YV[(f + 1) % 3] - YV[f];
+    len[f] = sqrt(dx * dx + dy * dy);
+  }
+  tgeo[e] = (4.0 * A) / ((len[0] + len[1]) + len[2]);
+  const double bx = (XV[0] + XV[1] + XV[2]) / 3.0, by = (YV[0] + YV[1] + YV[2]) / 3.0;
+  for (int i = 0; i < 3; i++) {
+    const double mx = 0.5 * (XV[i] + XV[(i + 1) % 3]), my = 0.5 * (YV[i] + YV[(i + 1) % 3]);
+    const double tx = mx - bx, ty = my - by;
+    const double tl = sqrt(tx * tx + ty * ty);
+    tgeo[(size_t)(1 + 2 * i) * K + e] = tx / tl;
+    tgeo[(size_t)(2 + 2 * i) * K + e] = ty / tl;
+  }
+}
+
 __global__ void k_scatter_field(int K, int Np, const int *orig, const double *src, double *dst) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
@@ -154,7 +179,7 @@ struct Ctx {
   std::vector<Ctx *> group;  // in-process peers (local transport), indexed by rank
   // device
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
-  double *dTalpha = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
+  double *dTalpha = nullptr, *dTgeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
   double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dRmin = nullptr;
   double *dXsBuf = nullptr, *dXrBuf = nullptr;
   int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
@@ -233,6 +258,7 @@ template <int N>
 static cudaError_t upload_ops(const RefOps &o) {
   Ops<N> h;
   constexpr int Np = Ops<N>::Np, Nc = Ops<N>::Nc, Ng = Ops<N>::Ng, Nfp = Ops<N>::Nfp;
+  if (o.Nc != Nc || o.Np != Np) return cudaErrorInvalidValue;  // host rule and kernel template disagree
   for (int c = 0; c < Nc; c++)
     for (int i = 0; i < Np; i++) {
       h.Ic[c][i] = o.Ic(c, i);
@@ -335,7 +361,8 @@ static double k1_bytes(int N, int nab, bool tvb) {
              9 * Nfp /*nbr Q faces*/ + 3 * Nfp /*nbr B faces*/ + 6 /*vertices*/ + 3 /*means w*/ + (tvb ? 9 : 0);
   return 8.0 * d + 12.0 /*E2E*/ + 1.0 /*dry flag*/;
 }
-static double k2_bytes() { return 8.0 * (3 + 9 + 9 + 6 + 6) + 12.0 + 4.0 + 4.0; }
+// own means, 3 neighbours' means, P1 midpoint data, alphas, static geometry (tgeo); E2E, pair code, 4 dry flags
+static double k2_bytes() { return 8.0 * (3 + 9 + 9 + 6 + 7) + 12.0 + 4.0 + 4.0; }
 
 static StepParams base_params(Ctx *c) {
   StepParams p;
@@ -348,6 +375,7 @@ static StepParams base_params(Ctx *c) {
   p.E2E = c->dE2E;
   p.tcode = c->dTcode;
   p.talpha = c->dTalpha;
+  p.tgeo = c->dTgeo;
   p.means = c->dMeans;
   p.dry = c->dDry;
   p.UT = c->dUT;
@@ -383,6 +411,7 @@ static int alloc_state(Ctx *c) {
   c->dMeans = (double *)c->dalloc(sizeof(double) * 3 * K);
   c->dUT = (double *)c->dalloc(sizeof(double) * 9 * K);
   c->dTalpha = (double *)c->dalloc(sizeof(double) * 6 * K);
+  c->dTgeo = (double *)c->dalloc(sizeof(double) * 7 * K);
   c->dAe = (double *)c->dalloc(sizeof(double) * Kin);
   c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * Kin);
   c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
@@ -627,6 +656,7 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   const size_t KNp = (size_t)c->Kin * c->Np;
   k_scatter_state<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp, c->dStage + 2 * KNp,
                                              c->dQ);
+  k_tvb_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dTgeo);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
   CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
@@ -1194,7 +1224,7 @@ void swe_destroy(swe_ctx *h) {
       for (auto &p : gq)
         if (p == c) p = nullptr;
     }
-  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha,
+  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo,
                   c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG,
                   c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
                   c->dXrIdx,   c->dDry,   c->dCounters};

@@ -74,20 +74,46 @@ def test_nodes(N):
 
 @pytest.mark.parametrize("N", range(1, 9))
 def test_cubature_exactness(N):
+    """P:81 + P:108-110 (reading A2'): symmetric rule of degree exactly 2N for N <= 5
+    (Dunavant sizes 3, 6, 12, 16, 25), collapsed Gauss-Jacobi of degree 2N+1 above."""
     re = oracle.refel(N)
     rc, sc, wc = re["rc"], re["sc"], re["wc"]
-    assert len(wc) == (N + 1) ** 2 and np.all(wc > 0)
+    sym = N <= 5
+    npts = {1: 3, 2: 6, 3: 12, 4: 16, 5: 25}[N] if sym else (N + 1) ** 2
+    strength = 2 * N if sym else 2 * N + 1
+    assert len(wc) == npts and np.all(wc > 0)
     assert abs(wc.sum() - 2.0) < 1e-14
     inside = (rc > -1) & (sc > -1) & (rc + sc < 0)
     assert inside.all()
-    for a in range(2 * N + 2):
-        for b in range(2 * N + 2 - a):
+    for a in range(strength + 1):
+        for b in range(strength + 1 - a):
             ex = float(tri_monomial_integral(a, b))
             assert abs(np.dot(wc, rc ** a * sc ** b) - ex) < 1e-13, (a, b)
-    # degree 2N+2 is not integrated exactly by every monomial (rule strength pinned)
-    errs = [abs(np.dot(wc, rc ** a * sc ** (2 * N + 2 - a)) - float(tri_monomial_integral(a, 2 * N + 2 - a)))
-            for a in range(2 * N + 3)]
+    # degree strength+1 is not integrated exactly by every monomial (rule strength pinned)
+    d = strength + 1
+    errs = [abs(np.dot(wc, rc ** a * sc ** (d - a)) - float(tri_monomial_integral(a, d - a))) for a in range(d + 1)]
     assert max(errs) > 1e-10
+
+
+@pytest.mark.parametrize("N", range(1, 6))
+def test_symmetric_cubature_orbits(N):
+    """The rule is fully symmetric: invariant (as a weighted point set) under the six
+    affine maps of the reference triangle onto itself (vertex permutations)."""
+    re = oracle.refel(N)
+    rc, sc, wc = re["rc"], re["sc"], re["wc"]
+    # barycentric of (r,s): l1 = -(r+s)/2, l2 = (1+r)/2, l3 = (1+s)/2
+    L = np.stack([-(rc + sc) / 2, (1 + rc) / 2, (1 + sc) / 2], 1)
+    key = lambda lam, w: sorted(zip(np.round(lam[:, 0], 12), np.round(lam[:, 1], 12), np.round(w, 12)))
+    base = key(L, wc)
+    import itertools
+    for perm in itertools.permutations(range(3)):
+        assert key(L[:, perm], wc) == base, perm
+    # Dunavant's published values (Table, degrees 2..10) agree to their printed digits
+    pub = {3: (0.116786275726379, 0.501426509658179), 4: (0.103217370534718, 0.658861384496480)}
+    if N in pub:
+        w, a = pub[N]
+        hit = np.isclose(L[:, 0], a, atol=1e-14) & np.isclose(L[:, 1], (1 - a) / 2, atol=1e-14)
+        assert hit.sum() == 1 and abs(wc[hit][0] / 2 - w) < 1e-14
 
 
 @pytest.mark.parametrize("N", range(1, 7))
@@ -109,11 +135,13 @@ def test_operators_exact_on_polynomials(N):
     qv = poly_eval(q, r, s)
     assert abs(qv @ re["Mref"] @ pv - poly_integral(poly_mul(p, q))) < 1e-12 * scale
     assert abs(re["wmean"].sum() - 2.0) < 1e-13
-    # P, Pr, Ps: v^T M (P F_c) = int v F, v^T M (Pr F_c) = int dv/dr F, for F of degree N+1
+    # P, Pr, Ps: v^T M (P F_c) = int v F for F of degree N, v^T M (Pr F_c) = int dv/dr F
+    # for F of degree N+1 (integrands of degree 2N: the cubature strength, A2')
+    M = re["Mref"]
+    F0 = random_poly(N, rng)
+    assert abs(qv @ M @ (re["P"] @ poly_eval(F0, re["rc"], re["sc"])) - poly_integral(poly_mul(q, F0))) < 1e-11 * scale
     F = random_poly(N + 1, rng)
     Fc = poly_eval(F, re["rc"], re["sc"])
-    M = re["Mref"]
-    assert abs(qv @ M @ (re["P"] @ Fc) - poly_integral(poly_mul(q, F))) < 1e-11 * scale
     assert abs(qv @ M @ (re["Pr"] @ Fc) - poly_integral(poly_mul(poly_dr(q), F))) < 1e-11 * scale * N
     assert abs(qv @ M @ (re["Ps"] @ Fc) - poly_integral(poly_mul(poly_ds(q), F))) < 1e-11 * scale * N
     # Lg: v^T M (Lg F_g) = sum over faces of int_{-1}^{1} v F dt (face parameter t)
