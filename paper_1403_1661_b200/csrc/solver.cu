@@ -54,6 +54,31 @@ __global__ void k_scatter_state(int K, int Np, const int *orig, const double *h,
   }
 }
 
+// K1 geometry table (K1_GEO == 2): the metric terms and face normals K1 would derive from the
+// vertices, with the same expressions.
+__global__ void k_geo(int K, const double *V, double *geo) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= K) return;
+  const double X[3] = {V[e], V[K + e], V[2 * (size_t)K + e]};
+  const double Y[3] = {V[3 * (size_t)K + e], V[4 * (size_t)K + e], V[5 * (size_t)K + e]};
+  const double xr = 0.5 * (X[1] - X[0]), xs = 0.5 * (X[2] - X[0]), yr = 0.5 * (Y[1] - Y[0]), ys = 0.5 * (Y[2] - Y[0]);
+  const double J = xr * ys - xs * yr;
+  const double rJ = 1.0 / J;
+  geo[e] = ys * rJ;
+  geo[K + e] = -xs * rJ;
+  geo[2 * (size_t)K + e] = -yr * rJ;
+  geo[3 * (size_t)K + e] = xr * rJ;
+  geo[4 * (size_t)K + e] = J;
+  for (int f = 0; f < 3; f++) {
+    const int f1 = f == 2 ? 0 : f + 1;
+    const double dx = X[f1] - X[f], dy = Y[f1] - Y[f];
+    const double len = sqrt(dx * dx + dy * dy);
+    geo[(size_t)(5 + 3 * f) * K + e] = dy / len;
+    geo[(size_t)(6 + 3 * f) * K + e] = -dx / len;
+    geo[(size_t)(7 + 3 * f) * K + e] = 0.5 * len * rJ;
+  }
+}
+
 // Static TVB geometry of every element (P:224-253 limiter stencil): Hk = 4A / perimeter
 // (level-binning geometry) and the unit vectors from the centroid to the three edge midpoints,
 // with the exact expressions K2 used when it derived them per launch.
@@ -179,7 +204,7 @@ struct Ctx {
   std::vector<Ctx *> group;  // in-process peers (local transport), indexed by rank
   // device
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
-  double *dTalpha = nullptr, *dTgeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
+  double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
   double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dRmin = nullptr;
   double *dXsBuf = nullptr, *dXrBuf = nullptr;
   int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
@@ -358,7 +383,8 @@ static void launch(int which, bool init, int N, const StepParams &p, cudaStream_
 static double k1_bytes(int N, int nab, bool tvb) {
   int Np = (N + 1) * (N + 2) / 2, Nfp = N + 1;
   double d = 3 * Np /*Q r*/ + 3 * Np /*Q w*/ + 3 * Np /*R w*/ + 3 * Np * (nab - 1) /*R r*/ + Np /*B*/ +
-             9 * Nfp /*nbr Q faces*/ + 3 * Nfp /*nbr B faces*/ + 6 /*vertices*/ + 3 /*means w*/ + (tvb ? 9 : 0);
+             9 * Nfp /*nbr Q faces*/ + 3 * Nfp /*nbr B faces*/ + (K1_GEO == 2 ? 14 /*geometry*/ : 6 /*vertices*/) +
+             3 /*means w*/ + (tvb ? 9 : 0);
   return 8.0 * d + 12.0 /*E2E*/ + 1.0 /*dry flag*/;
 }
 // own means, 3 neighbours' means, P1 midpoint data, alphas, static geometry (tgeo); E2E, pair code, 4 dry flags
@@ -376,6 +402,7 @@ static StepParams base_params(Ctx *c) {
   p.tcode = c->dTcode;
   p.talpha = c->dTalpha;
   p.tgeo = c->dTgeo;
+  p.geo = c->dGeo;
   p.means = c->dMeans;
   p.dry = c->dDry;
   p.UT = c->dUT;
@@ -412,6 +439,9 @@ static int alloc_state(Ctx *c) {
   c->dUT = (double *)c->dalloc(sizeof(double) * 9 * K);
   c->dTalpha = (double *)c->dalloc(sizeof(double) * 6 * K);
   c->dTgeo = (double *)c->dalloc(sizeof(double) * 7 * K);
+#if K1_GEO == 2
+  c->dGeo = (double *)c->dalloc(sizeof(double) * 14 * K);
+#endif
   c->dAe = (double *)c->dalloc(sizeof(double) * Kin);
   c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * Kin);
   c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
@@ -657,6 +687,9 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   k_scatter_state<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp, c->dStage + 2 * KNp,
                                              c->dQ);
   k_tvb_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dTgeo);
+#if K1_GEO == 2
+  k_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dGeo);
+#endif
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
   CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
@@ -1224,7 +1257,7 @@ void swe_destroy(swe_ctx *h) {
       for (auto &p : gq)
         if (p == c) p = nullptr;
     }
-  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo,
+  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo,
                   c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG,
                   c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
                   c->dXrIdx,   c->dDry,   c->dCounters};
