@@ -272,9 +272,11 @@ def main():
             roof["traffic"] = tr["bytes_per_launch"]
             roof["traffic_launch_elements"] = tr["elements"]
             roof["traffic_bytes_per_elem_update"] = tr["bytes_per_elem_update"]
-            roof["algorithmic_bytes_per_elem_update"] = tr["algorithmic_bytes_per_elem_update"]
         except Exception:
             pass
+    k1_updates = U * args.steps / (3 * Np)  # element updates of this rank (K1 launches)
+    if k1_updates:
+        roof["algorithmic_bytes_per_elem_update"] = prof["k1_bytes"] / k1_updates
 
     info = s.info()
 

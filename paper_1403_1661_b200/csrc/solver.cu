@@ -204,10 +204,10 @@ struct Ctx {
   std::vector<Ctx *> group;  // in-process peers (local transport), indexed by rank
   // device
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
-  double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
+  double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dBg = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
   double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dRmin = nullptr;
   double *dXsBuf = nullptr, *dXrBuf = nullptr;
-  int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
+  int *dE2E = nullptr, *dNlev3 = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
   size_t xcap = 0;  // capacity (entries) of the exchange index/buffer arrays
   unsigned char *dDry = nullptr;
   unsigned long long *dCounters = nullptr;
@@ -353,6 +353,14 @@ static void launch_k1(const StepParams &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
   size_t smem = INIT ? 0 : sizeof(double) * SmemOps<N>::total;
+#if K1_TMA_HIST
+  if (!INIT) smem += sizeof(double) * (2 + (size_t)2 * 3 * SmemOps<N>::Np * kHistRow);
+  static bool attr_set = false;  // one per template instance
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_rhs_update<N, INIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+#endif
   k_rhs_update<N, INIT><<<(n + 127) / 128, 128, smem, s>>>(p);
 }
 template <int N>
@@ -383,9 +391,9 @@ static void launch(int which, bool init, int N, const StepParams &p, cudaStream_
 static double k1_bytes(int N, int nab, bool tvb) {
   int Np = (N + 1) * (N + 2) / 2, Nfp = N + 1;
   double d = 3 * Np /*Q r*/ + 3 * Np /*Q w*/ + 3 * Np /*R w*/ + 3 * Np * (nab - 1) /*R r*/ + Np /*B*/ +
-             9 * Nfp /*nbr Q faces*/ + 3 * Nfp /*nbr B faces*/ + (K1_GEO == 2 ? 14 /*geometry*/ : 6 /*vertices*/) +
+             9 * Nfp /*nbr Q faces*/ + (K1_BG ? 6 * Nfp /*B at Gauss points*/ : 3 * Nfp /*nbr B faces*/) + (K1_GEO == 2 ? 14 /*geometry*/ : 6 /*vertices*/) +
              3 /*means w*/ + (tvb ? 9 : 0);
-  return 8.0 * d + 12.0 /*E2E*/ + 1.0 /*dry flag*/;
+  return 8.0 * d + 12.0 /*E2E*/ + (K1_NLEV ? 4.0 : 0.0) /*neighbour levels*/ + 1.0 /*dry flag*/;
 }
 // own means, 3 neighbours' means, P1 midpoint data, alphas, static geometry (tgeo); E2E, pair code, 4 dry flags
 static double k2_bytes() { return 8.0 * (3 + 9 + 9 + 6 + 7) + 12.0 + 4.0 + 4.0; }
@@ -400,9 +408,11 @@ static StepParams base_params(Ctx *c) {
   p.V = c->dV;
   p.E2E = c->dE2E;
   p.tcode = c->dTcode;
+  p.nlev3 = c->dNlev3;
   p.talpha = c->dTalpha;
   p.tgeo = c->dTgeo;
   p.geo = c->dGeo;
+  p.bg = c->dBg;
   p.means = c->dMeans;
   p.dry = c->dDry;
   p.UT = c->dUT;
@@ -442,10 +452,14 @@ static int alloc_state(Ctx *c) {
 #if K1_GEO == 2
   c->dGeo = (double *)c->dalloc(sizeof(double) * 14 * K);
 #endif
+#if K1_BG
+  c->dBg = (double *)c->dalloc(sizeof(double) * 2 * 3 * (c->N + 1) * K);
+#endif
   c->dAe = (double *)c->dalloc(sizeof(double) * Kin);
   c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * Kin);
   c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
   c->dTcode = (int *)c->dalloc(sizeof(int) * K);
+  c->dNlev3 = (int *)c->dalloc(sizeof(int) * K);
   c->dOrig = (int *)c->dalloc(sizeof(int) * K);
   c->dDry = (unsigned char *)c->dalloc(K);
   c->dPartials = (double *)c->dalloc(sizeof(double) * 2 * ((K + 255) / 256));
@@ -640,7 +654,7 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
     }
   }
   std::vector<double> V((size_t)6 * K, 0.0), TA((size_t)6 * K, 0.0);
-  std::vector<int> E2E((size_t)3 * K), TC(K, 0);
+  std::vector<int> E2E((size_t)3 * K), TC(K, 0), NL(K, 0);
   for (int k = 0; k < K; k++) {
     int e = c->order[k];
     const int32_t *v = &c->mesh.etov[(size_t)3 * e];
@@ -657,6 +671,7 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
           return SWE_ERR_MESH;
         }
         E2E[(size_t)f * K + k] = (inv[n] << 2) | nf;
+        NL[k] |= ((levels[n] - 1) & 7) << (3 * f);
       } else {
         E2E[(size_t)f * K + k] = (k << 2) | f;  // ghosts are never launched
       }
@@ -675,6 +690,7 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   CK(cudaMemcpyAsync(c->dTalpha, TA.data(), sizeof(double) * TA.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dE2E, E2E.data(), sizeof(int) * E2E.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dTcode, TC.data(), sizeof(int) * TC.size(), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dNlev3, NL.data(), sizeof(int) * NL.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dOrig, c->order.data(), sizeof(int) * K, cudaMemcpyHostToDevice, c->stream));
   if (!xsf.empty())
     CK(cudaMemcpyAsync(c->dXsIdx, xsf.data(), sizeof(int) * xsf.size(), cudaMemcpyHostToDevice, c->stream));
@@ -689,6 +705,18 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   k_tvb_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dTgeo);
 #if K1_GEO == 2
   k_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dGeo);
+#endif
+#if K1_BG
+  {
+    StepParams bp = base_params(c);
+    const int nbo = (c->kown + 127) / 128;
+    if (nbo > 0) switch (c->N) {
+        case 1: k_bgauss<1><<<nbo, 128, 0, c->stream>>>(bp); break;
+        case 2: k_bgauss<2><<<nbo, 128, 0, c->stream>>>(bp); break;
+        case 3: k_bgauss<3><<<nbo, 128, 0, c->stream>>>(bp); break;
+        case 4: k_bgauss<4><<<nbo, 128, 0, c->stream>>>(bp); break;
+      }
+  }
 #endif
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
@@ -1257,9 +1285,9 @@ void swe_destroy(swe_ctx *h) {
       for (auto &p : gq)
         if (p == c) p = nullptr;
     }
-  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo,
+  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo, c->dBg,
                   c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG,
-                  c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
+                  c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dNlev3, c->dTcode,   c->dOrig,  c->dXsIdx,
                   c->dXrIdx,   c->dDry,   c->dCounters};
   for (void *p : ptrs) c->dfree(p);
   if (c->hCounters) cudaFreeHost(c->hCounters);
