@@ -54,7 +54,7 @@ __global__ void k_scatter_state(int K, int Np, const int *orig, const double *h,
   }
 }
 
-// K1 geometry table (K1_GEO == 2): the metric terms and face normals K1 would derive from the
+// K1 geometry table: the metric terms and face normals K1 would derive from the
 // vertices, with the same expressions.
 __global__ void k_geo(int K, const double *V, double *geo) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -204,10 +204,10 @@ struct Ctx {
   std::vector<Ctx *> group;  // in-process peers (local transport), indexed by rank
   // device
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
-  double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dBg = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
+  double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
   double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dRmin = nullptr;
   double *dXsBuf = nullptr, *dXrBuf = nullptr;
-  int *dE2E = nullptr, *dNlev3 = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
+  int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
   size_t xcap = 0;  // capacity (entries) of the exchange index/buffer arrays
   unsigned char *dDry = nullptr;
   unsigned long long *dCounters = nullptr;
@@ -215,6 +215,7 @@ struct Ctx {
   double *hInjected = nullptr;              // pinned
   // state / schedule
   bool have_state = false, materialized = false, scheduled = false;
+  bool layout_valid = false;  // internal order + static tables match c->level / c->L
   double dt = 0.0;
   int L = 1;
   std::vector<int32_t> level;  // given-mesh order
@@ -353,15 +354,19 @@ static void launch_k1(const StepParams &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
   size_t smem = INIT ? 0 : sizeof(double) * SmemOps<N>::total;
-#if K1_TMA_HIST
-  if (!INIT) smem += sizeof(double) * (2 + (size_t)2 * 3 * SmemOps<N>::Np * kHistRow);
-  static bool attr_set = false;  // one per template instance
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_rhs_update<N, INIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
+  int grid = (n + 127) / 128;
+#if K1_PERSIST
+  static int resident = 0;  // one per template instance: SMs x resident blocks per SM
+  if (resident == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update<N, INIT>, 128, smem);
+    resident = std::max(1, sms * per_sm);
   }
+  grid = std::min(grid, resident);
 #endif
-  k_rhs_update<N, INIT><<<(n + 127) / 128, 128, smem, s>>>(p);
+  k_rhs_update<N, INIT><<<grid, 128, smem, s>>>(p);
 }
 template <int N>
 static void launch_k2(const StepParams &p, cudaStream_t s) {
@@ -391,9 +396,8 @@ static void launch(int which, bool init, int N, const StepParams &p, cudaStream_
 static double k1_bytes(int N, int nab, bool tvb) {
   int Np = (N + 1) * (N + 2) / 2, Nfp = N + 1;
   double d = 3 * Np /*Q r*/ + 3 * Np /*Q w*/ + 3 * Np /*R w*/ + 3 * Np * (nab - 1) /*R r*/ + Np /*B*/ +
-             9 * Nfp /*nbr Q faces*/ + (K1_BG ? 6 * Nfp /*B at Gauss points*/ : 3 * Nfp /*nbr B faces*/) + (K1_GEO == 2 ? 14 /*geometry*/ : 6 /*vertices*/) +
-             3 /*means w*/ + (tvb ? 9 : 0);
-  return 8.0 * d + 12.0 /*E2E*/ + (K1_NLEV ? 4.0 : 0.0) /*neighbour levels*/ + 1.0 /*dry flag*/;
+             9 * Nfp /*nbr Q faces*/ + 3 * Nfp /*nbr B faces*/ + 14 /*geometry table*/ + 3 /*means w*/ + (tvb ? 9 : 0);
+  return 8.0 * d + 12.0 /*E2E*/ + 1.0 /*dry flag*/;
 }
 // own means, 3 neighbours' means, P1 midpoint data, alphas, static geometry (tgeo); E2E, pair code, 4 dry flags
 static double k2_bytes() { return 8.0 * (3 + 9 + 9 + 6 + 7) + 12.0 + 4.0 + 4.0; }
@@ -408,11 +412,9 @@ static StepParams base_params(Ctx *c) {
   p.V = c->dV;
   p.E2E = c->dE2E;
   p.tcode = c->dTcode;
-  p.nlev3 = c->dNlev3;
   p.talpha = c->dTalpha;
   p.tgeo = c->dTgeo;
   p.geo = c->dGeo;
-  p.bg = c->dBg;
   p.means = c->dMeans;
   p.dry = c->dDry;
   p.UT = c->dUT;
@@ -449,17 +451,11 @@ static int alloc_state(Ctx *c) {
   c->dUT = (double *)c->dalloc(sizeof(double) * 9 * K);
   c->dTalpha = (double *)c->dalloc(sizeof(double) * 6 * K);
   c->dTgeo = (double *)c->dalloc(sizeof(double) * 7 * K);
-#if K1_GEO == 2
   c->dGeo = (double *)c->dalloc(sizeof(double) * 14 * K);
-#endif
-#if K1_BG
-  c->dBg = (double *)c->dalloc(sizeof(double) * 2 * 3 * (c->N + 1) * K);
-#endif
   c->dAe = (double *)c->dalloc(sizeof(double) * Kin);
   c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * Kin);
   c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
   c->dTcode = (int *)c->dalloc(sizeof(int) * K);
-  c->dNlev3 = (int *)c->dalloc(sizeof(int) * K);
   c->dOrig = (int *)c->dalloc(sizeof(int) * K);
   c->dDry = (unsigned char *)c->dalloc(K);
   c->dPartials = (double *)c->dalloc(sizeof(double) * 2 * ((K + 255) / 256));
@@ -612,8 +608,13 @@ static void order_subset(const HostMesh &m, const std::vector<int32_t> &levels, 
 // Build the internal order for `levels` (given-mesh order), upload static data,
 // scatter the staged unlimited state, reset the MRAB schedule.  The initial
 // limiting (Alg. 2 line 1) is applied by init_limit_* (group-aware).
+static int materialize_state(Ctx *c);
 static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   const int K = c->K;
+  // The layout (internal order, connectivity, geometry, exchange tables) depends only on the
+  // levels: a new state that bins to the resident levels reuses it and only scatters the state.
+  if (c->layout_valid && c->L == L && c->level == levels) return materialize_state(c);
+  c->layout_valid = false;
   c->level = levels;
   c->L = L;
   std::vector<int32_t> owned_sorted, ghosts_sorted;
@@ -654,7 +655,7 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
     }
   }
   std::vector<double> V((size_t)6 * K, 0.0), TA((size_t)6 * K, 0.0);
-  std::vector<int> E2E((size_t)3 * K), TC(K, 0), NL(K, 0);
+  std::vector<int> E2E((size_t)3 * K), TC(K, 0);
   for (int k = 0; k < K; k++) {
     int e = c->order[k];
     const int32_t *v = &c->mesh.etov[(size_t)3 * e];
@@ -671,7 +672,6 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
           return SWE_ERR_MESH;
         }
         E2E[(size_t)f * K + k] = (inv[n] << 2) | nf;
-        NL[k] |= ((levels[n] - 1) & 7) << (3 * f);
       } else {
         E2E[(size_t)f * K + k] = (k << 2) | f;  // ghosts are never launched
       }
@@ -690,7 +690,6 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   CK(cudaMemcpyAsync(c->dTalpha, TA.data(), sizeof(double) * TA.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dE2E, E2E.data(), sizeof(int) * E2E.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dTcode, TC.data(), sizeof(int) * TC.size(), cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->dNlev3, NL.data(), sizeof(int) * NL.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dOrig, c->order.data(), sizeof(int) * K, cudaMemcpyHostToDevice, c->stream));
   if (!xsf.empty())
     CK(cudaMemcpyAsync(c->dXsIdx, xsf.data(), sizeof(int) * xsf.size(), cudaMemcpyHostToDevice, c->stream));
@@ -699,25 +698,21 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   CK(cudaStreamSynchronize(c->stream));  // host vectors above are released on return
   int nb = (K + 127) / 128;
   k_scatter_field<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dBcaller, c->dB);
+  k_tvb_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dTgeo);
+  k_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dGeo);
+  CK(cudaGetLastError());
+  c->layout_valid = true;
+  return materialize_state(c);
+}
+
+// State part of materialize: the staged caller-order state into the internal order, fresh
+// dry flags, counters, AB ramp and clocks.
+static int materialize_state(Ctx *c) {
+  const int K = c->K;
+  const int nb = (K + 127) / 128;
   const size_t KNp = (size_t)c->Kin * c->Np;
   k_scatter_state<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp, c->dStage + 2 * KNp,
                                              c->dQ);
-  k_tvb_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dTgeo);
-#if K1_GEO == 2
-  k_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dGeo);
-#endif
-#if K1_BG
-  {
-    StepParams bp = base_params(c);
-    const int nbo = (c->kown + 127) / 128;
-    if (nbo > 0) switch (c->N) {
-        case 1: k_bgauss<1><<<nbo, 128, 0, c->stream>>>(bp); break;
-        case 2: k_bgauss<2><<<nbo, 128, 0, c->stream>>>(bp); break;
-        case 3: k_bgauss<3><<<nbo, 128, 0, c->stream>>>(bp); break;
-        case 4: k_bgauss<4><<<nbo, 128, 0, c->stream>>>(bp); break;
-      }
-  }
-#endif
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
   CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
@@ -1285,9 +1280,9 @@ void swe_destroy(swe_ctx *h) {
       for (auto &p : gq)
         if (p == c) p = nullptr;
     }
-  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo, c->dBg,
+  void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo,
                   c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG,
-                  c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dNlev3, c->dTcode,   c->dOrig,  c->dXsIdx,
+                  c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
                   c->dXrIdx,   c->dDry,   c->dCounters};
   for (void *p : ptrs) c->dfree(p);
   if (c->hCounters) cudaFreeHost(c->hCounters);

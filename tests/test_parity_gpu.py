@@ -212,3 +212,37 @@ def test_ragged_level_ranges_many_levels():
     o, s, _ = run_both(w, 2, dt, nlevels=8)
     assert np.array_equal(o.levels(), s.levels())
     assert_parity(o, s, w.g)
+
+
+def test_set_state_again_reuses_or_rebuilds_layout():
+    """swe_set_state on a live context: a state that bins to the resident levels reuses the internal
+    layout (only the state is scattered) and must reproduce a fresh run bit for bit; a state that bins
+    to other levels rebuilds the layout and must match the oracle."""
+    w = si.c4_dambreak(N=2, base=5)
+    m = w.mesh
+    o, s, d = make_pair(w)
+    dt = si.dt_for(m, w.N, w.g, 1.875, 13.0, 0.2)
+    s.set_state(d["h"], d["hu"], d["hv"])
+    for _ in range(3):
+        s.step(dt, 3)
+    first = s.get_state()
+    lev1 = s.levels()
+    s.set_state(d["h"], d["hu"], d["hv"])  # same state -> same levels -> layout reused
+    for _ in range(3):
+        s.step(dt, 3)
+    again = s.get_state()
+    assert np.array_equal(s.levels(), lev1)
+    for a, b in zip(first, again):
+        assert np.array_equal(a, b)
+    # a local jet in the reservoir (speeds above a_floor = 13 m/s) moves elements to finer levels ->
+    # layout rebuilt; set_state resets the schedule, so a smaller dt is allowed
+    x, y = P.nodes(m.vx, m.vy, m.etov, w.N)
+    h2, hu2, hv2 = d["h"], d["hu"] + 20.0 * np.exp(-((x - 8.0) ** 2 + (y - 15.0) ** 2) / 20.0) * d["h"], d["hv"]
+    s.set_state(h2, hu2, hv2)
+    o.set_state(h2, hu2, hv2)
+    for _ in range(3):
+        s.step(0.5 * dt, 3)
+        assert o.step(0.5 * dt, 3) == 0
+    assert np.array_equal(s.levels(), o.levels())
+    assert not np.array_equal(s.levels(), lev1)
+    assert_parity(o, s, w.g)
