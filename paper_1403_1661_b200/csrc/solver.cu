@@ -354,19 +354,19 @@ static void launch_k1(const StepParams &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
   size_t smem = INIT ? 0 : sizeof(double) * SmemOps<N>::total;
-  int grid = (n + 127) / 128;
+  int grid = (n + K1_BLOCK - 1) / K1_BLOCK;
 #if K1_PERSIST
   static int resident = 0;  // one per template instance: SMs x resident blocks per SM
   if (resident == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update<N, INIT>, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update<N, INIT>, K1_BLOCK, smem);
     resident = std::max(1, sms * per_sm);
   }
   grid = std::min(grid, resident);
 #endif
-  k_rhs_update<N, INIT><<<grid, 128, smem, s>>>(p);
+  k_rhs_update<N, INIT><<<grid, K1_BLOCK, smem, s>>>(p);
 }
 template <int N>
 static void launch_k2(const StepParams &p, cudaStream_t s) {
