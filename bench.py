@@ -167,6 +167,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--order", type=int, default=3, help="polynomial order N of the GPU arm (headline: 3)")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -211,7 +212,8 @@ def main():
         owner = None
         part = {}
     m = w.mesh
-    N, Np, L = 3, 10, w.nlevels
+    N, L = args.order, w.nlevels
+    Np = (N + 1) * (N + 2) // 2
     x, y = P.nodes(m.vx, m.vy, m.etov, N)
     B, h, hu, hv = w.fields(x, y)
     del x, y
@@ -262,11 +264,11 @@ def main():
     peak, peak_kind = load_peaks()
     k1_gbs = prof["k1_bytes"] / (prof["k1_ms"] / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
-            "traffic": None, "kernel": "k_rhs_update<3>", "peak_kind": peak_kind,
+            "traffic": None, "kernel": f"k_rhs_update<{N}>", "peak_kind": peak_kind,
             "k1_share_of_step": prof["k1_ms"] / ms if ms > 0 else None,
             "k2_share_of_step": prof["k2_ms"] / ms if ms > 0 else None}
     traffic_path = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
-    if os.path.exists(traffic_path):  # one ncu --set full capture (profiles/), not measured in this run
+    if N == 3 and os.path.exists(traffic_path):  # one ncu --set full capture (profiles/), not measured here
         try:
             tr = json.load(open(traffic_path))
             roof["traffic"] = tr["bytes_per_launch"]
@@ -328,10 +330,11 @@ def main():
         cpu = cpu_baseline(args)
     if rank == 0:
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC.replace("N=3", f"N={N}"), "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C5 synthetic tsunami basin (SURVEY 8(d)), N=3, 4 MRAB levels, PP+TVB"
+            "config": {"workload": f"C5 synthetic tsunami basin (SURVEY 8(d)), N={N}, 4 MRAB levels, PP+TVB"
                                    + (f", {world} y-strips (weak scaling, NCCL halo exchange)" if world > 1 else ""),
                        "K_per_rank": int(len(lev)), "level_counts": [int(c) for c in np.bincount(lev, minlength=L + 1)[1:]],
                        "dof_updates_per_step": U_all, "dt": dt, "l2": "inputs larger than L2 (state+history ~13 GB/rank)",

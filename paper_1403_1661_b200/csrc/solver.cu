@@ -327,6 +327,24 @@ static std::vector<double> smem_ops(const RefOps &o) {
     for (int i = 0; i < SO::Np; i++) v[SO::LgT + g * SO::NpP + i] = o.Lg(i, g);
   for (int j = 0; j < SO::Ng; j++)
     for (int k = 0; k < SO::Nfp; k++) v[SO::Ig1 + j * SO::NfpP + k] = o.Ig1(j, k);
+  // DMMA fragments (K1_MMA)
+  const DMat *icops[3] = {&o.Ic, &o.IcDr, &o.IcDs}, *pops[3] = {&o.Pr, &o.Ps, &o.P};
+  for (int op = 0; op < 3; op++)
+    for (int ks = 0; ks < SO::NKN; ks++)
+      for (int nt = 0; nt < SO::NTP; nt++)
+        for (int l = 0; l < 32; l++) {
+          const int pt = 8 * nt + l / 4, node = 4 * ks + l % 4;
+          v[SO::FIc + ((op * SO::NKN + ks) * SO::NTP + nt) * 32 + l] =
+              (pt < SO::Nc && node < SO::Np) ? (*icops[op])(pt, node) : 0.0;
+        }
+  for (int op = 0; op < 3; op++)
+    for (int ks = 0; ks < SO::NKP; ks++)
+      for (int nt = 0; nt < SO::NTN; nt++)
+        for (int l = 0; l < 32; l++) {
+          const int node = 8 * nt + l / 4, pt = 4 * ks + l % 4;
+          v[SO::FP + ((op * SO::NKP + ks) * SO::NTN + nt) * 32 + l] =
+              (pt < SO::Nc && node < SO::Np) ? (*pops[op])(node, pt) : 0.0;
+        }
   return v;
 }
 static std::vector<double> smem_ops_any(const RefOps &o) {
@@ -353,7 +371,7 @@ template <int N, bool INIT>
 static void launch_k1(const StepParams &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
-  size_t smem = INIT ? 0 : sizeof(double) * SmemOps<N>::total;
+  size_t smem = INIT ? 0 : sizeof(double) * SmemOps<N>::scalar_total;
   int grid = (n + K1_BLOCK - 1) / K1_BLOCK;
 #if K1_PERSIST
   static int resident = 0;  // one per template instance: SMs x resident blocks per SM
@@ -366,6 +384,16 @@ static void launch_k1(const StepParams &p, cudaStream_t s) {
   }
   grid = std::min(grid, resident);
 #endif
+  if (!INIT && N >= K1_MMA_MIN_N) {
+    const size_t smem_mma = sizeof(double) * (SmemOps<N>::total + (size_t)(4 * SmemOps<N>::Np + 1) * (K1_BLOCK + kTilePad));
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_rhs_update_mma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mma);
+      attr = true;
+    }
+    k_rhs_update_mma<N><<<(n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem_mma, s>>>(p);
+    return;
+  }
   k_rhs_update<N, INIT><<<grid, K1_BLOCK, smem, s>>>(p);
 }
 template <int N>

@@ -120,6 +120,17 @@ def test_parity_mrab_dambreak(nlevels):
     assert_parity(o, s, w.g)
 
 
+def test_parity_mrab_dambreak_n4_tensor_path():
+    """N = 4 runs the volume term on the FP64 tensor path (DMMA, k_rhs_update_mma): C4 wet/dry with
+    PP + TVB and 3 MRAB levels against the oracle."""
+    w = si.c4_dambreak(N=4, base=5)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    o, s, _ = run_both(w, 8, dt, nlevels=3)
+    assert np.array_equal(o.levels(), s.levels())
+    assert_parity(o, s, w.g)
+    assert s.info()["n_pp"] == o.info()["n_pp"] > 0
+
+
 def test_parity_mrab_smooth_wet():
     """Dense-output coupling without limiter decisions: fully wet graded C4 mesh, smooth hump, 3 levels."""
     w = si.c4_dambreak(N=3, base=5)

@@ -14,8 +14,11 @@ fname = None
 for r in rows:
     if r and r[0] == "File Path":
         fname = r[1].split("/")[-1]
-    if len(r) > col and r[0] not in ("", "Line No", "File Path", "Function Name") and r[col] not in ("-", ""):
-        lines.append((float(r[col]), fname, int(r[0]), r[1].strip()))
+    if len(r) > col and r[0].isdigit() and r[col] not in ("-", ""):
+        try:
+            lines.append((float(r[col]), fname, int(r[0]), r[1].strip()))
+        except ValueError:
+            pass
 tot = sum(v for v, *_ in lines)
 print("column", hdr[col], "total", tot)
 for v, f, ln, src in sorted(lines, reverse=True)[:top]:
