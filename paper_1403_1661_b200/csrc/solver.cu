@@ -333,7 +333,10 @@ static std::vector<double> smem_ops(const RefOps &o) {
     for (int ks = 0; ks < SO::NKN; ks++)
       for (int nt = 0; nt < SO::NTP; nt++)
         for (int l = 0; l < 32; l++) {
-          const int pt = 8 * nt + l / 4, node = 4 * ks + l % 4;
+          // column j = l / 4 of n-tile nt carries point 4 (2 nt + (j & 1)) + (j >> 1): lane l of the accumulator
+          // (columns 2 (l % 4) + i) then holds exactly the points 4 ks + l % 4, ks = 2 nt + i, that its projection
+          // A fragments need, so no shuffles are required between the two contractions
+          const int j = l / 4, pt = 4 * (2 * nt + (j & 1)) + (j >> 1), node = 4 * ks + l % 4;
           v[SO::FIc + ((op * SO::NKN + ks) * SO::NTP + nt) * 32 + l] =
               (pt < SO::Nc && node < SO::Np) ? (*icops[op])(pt, node) : 0.0;
         }
@@ -385,7 +388,8 @@ static void launch_k1(const StepParams &p, cudaStream_t s) {
   grid = std::min(grid, resident);
 #endif
   if (!INIT && N >= K1_MMA_MIN_N) {
-    const size_t smem_mma = sizeof(double) * (SmemOps<N>::total + (size_t)(4 * SmemOps<N>::Np + 1) * (K1_BLOCK + kTilePad));
+    const size_t smem_mma =
+        sizeof(double) * (SmemOps<N>::total + (K1_MMA_TILE ? (size_t)(4 * SmemOps<N>::Np + 1) * (K1_BLOCK + kTilePad) : 0));
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_rhs_update_mma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mma);
