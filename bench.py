@@ -168,6 +168,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--order", type=int, default=3, help="polynomial order N of the GPU arm (headline: 3)")
+    ap.add_argument("--precision", type=int, default=64, choices=(32, 64),
+                    help="device arithmetic of the GPU arm (headline: 64; 32 = FP32 variant, SURVEY NEXT-2)")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -217,7 +219,8 @@ def main():
     x, y = P.nodes(m.vx, m.vy, m.etov, N)
     B, h, hu, hv = w.fields(x, y)
     del x, y
-    s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=w.params, device=local, **part)
+    s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=dict(w.params, precision=args.precision), device=local,
+                 **part)
     dt = si.dt_for(m, N, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
     if world > 1:
         tdt = torch.tensor([dt], device="cuda", dtype=torch.float64)
@@ -268,7 +271,7 @@ def main():
             "k1_share_of_step": prof["k1_ms"] / ms if ms > 0 else None,
             "k2_share_of_step": prof["k2_ms"] / ms if ms > 0 else None}
     traffic_path = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
-    if N == 3 and os.path.exists(traffic_path):  # one ncu --set full capture (profiles/), not measured here
+    if N == 3 and args.precision == 64 and os.path.exists(traffic_path):  # ncu capture (profiles/), not this run
         try:
             tr = json.load(open(traffic_path))
             roof["traffic"] = tr["bytes_per_launch"]
@@ -330,10 +333,11 @@ def main():
         cpu = cpu_baseline(args)
     if rank == 0:
         out = {
-            "metric": METRIC.replace("N=3", f"N={N}"), "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC.replace("N=3", f"N={N}").replace("FP64", "FP64" if args.precision == 64 else "FP32"),
+            "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
             "config": {"workload": f"C5 synthetic tsunami basin (SURVEY 8(d)), N={N}, 4 MRAB levels, PP+TVB"
                                    + (f", {world} y-strips (weak scaling, NCCL halo exchange)" if world > 1 else ""),
                        "K_per_rank": int(len(lev)), "level_counts": [int(c) for c in np.bincount(lev, minlength=L + 1)[1:]],

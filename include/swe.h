@@ -26,7 +26,8 @@
  *   - Errors are negative return codes; nothing aborts.  The message of the
  *     last error of a context is available from swe_last_error().
  *   - A context is not thread-safe; distinct contexts are independent.
- *   - Arithmetic is IEEE binary64 throughout (device and host).
+ *   - Arithmetic is IEEE binary64 throughout (device and host), unless swe_params.precision
+ *     selects the FP32 variant for the device state and kernels.
  */
 #ifndef SWE_H
 #define SWE_H
@@ -95,6 +96,11 @@ typedef struct {
   const int32_t *owner;
   const int64_t *gid;
   const void *nccl_id;
+  /* Arithmetic precision of the device state and kernels: 64 (or 0, default) = IEEE binary64; 32 = the
+   * FP32 variant: state, history and kernels in binary32, host arrays still double,
+   * level binning still from the binary64 input (bit-exact); parity target 1e-5 against the FP64 oracle
+   * (DESIGN.md).  Other values: SWE_ERR_ARG. */
+  int32_t precision;
 } swe_params;
 
 typedef struct {

@@ -42,21 +42,23 @@ __global__ void k_speeds(int K, int Np, double g, double e4, double a_floor, con
 }
 
 // caller layout [K][Np] (3 arrays) -> internal [3][Np][K] in internal order
+template <typename T>
 __global__ void k_scatter_state(int K, int Np, const int *orig, const double *h, const double *hu, const double *hv,
-                                double *Q) {
+                                T *Q) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   size_t e = (size_t)orig[k];
   for (int i = 0; i < Np; i++) {
-    Q[(size_t)i * K + k] = h[e * Np + i];
-    Q[(size_t)(Np + i) * K + k] = hu[e * Np + i];
-    Q[(size_t)(2 * Np + i) * K + k] = hv[e * Np + i];
+    Q[(size_t)i * K + k] = (T)h[e * Np + i];
+    Q[(size_t)(Np + i) * K + k] = (T)hu[e * Np + i];
+    Q[(size_t)(2 * Np + i) * K + k] = (T)hv[e * Np + i];
   }
 }
 
 // K1 geometry table: the metric terms and face normals K1 would derive from the
 // vertices, with the same expressions.
-__global__ void k_geo(int K, const double *V, double *geo) {
+template <typename T>
+__global__ void k_geo(int K, const double *V, T *geo) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= K) return;
   const double X[3] = {V[e], V[K + e], V[2 * (size_t)K + e]};
@@ -64,25 +66,26 @@ __global__ void k_geo(int K, const double *V, double *geo) {
   const double xr = 0.5 * (X[1] - X[0]), xs = 0.5 * (X[2] - X[0]), yr = 0.5 * (Y[1] - Y[0]), ys = 0.5 * (Y[2] - Y[0]);
   const double J = xr * ys - xs * yr;
   const double rJ = 1.0 / J;
-  geo[e] = ys * rJ;
-  geo[K + e] = -xs * rJ;
-  geo[2 * (size_t)K + e] = -yr * rJ;
-  geo[3 * (size_t)K + e] = xr * rJ;
-  geo[4 * (size_t)K + e] = J;
+  geo[e] = (T)(ys * rJ);
+  geo[K + e] = (T)(-xs * rJ);
+  geo[2 * (size_t)K + e] = (T)(-yr * rJ);
+  geo[3 * (size_t)K + e] = (T)(xr * rJ);
+  geo[4 * (size_t)K + e] = (T)J;
   for (int f = 0; f < 3; f++) {
     const int f1 = f == 2 ? 0 : f + 1;
     const double dx = X[f1] - X[f], dy = Y[f1] - Y[f];
     const double len = sqrt(dx * dx + dy * dy);
-    geo[(size_t)(5 + 3 * f) * K + e] = dy / len;
-    geo[(size_t)(6 + 3 * f) * K + e] = -dx / len;
-    geo[(size_t)(7 + 3 * f) * K + e] = 0.5 * len * rJ;
+    geo[(size_t)(5 + 3 * f) * K + e] = (T)(dy / len);
+    geo[(size_t)(6 + 3 * f) * K + e] = (T)(-dx / len);
+    geo[(size_t)(7 + 3 * f) * K + e] = (T)(0.5 * len * rJ);
   }
 }
 
 // Static TVB geometry of every element (P:224-253 limiter stencil): Hk = 4A / perimeter
 // (level-binning geometry) and the unit vectors from the centroid to the three edge midpoints,
 // with the exact expressions K2 used when it derived them per launch.
-__global__ void k_tvb_geo(int K, const double *V, double *tgeo) {
+template <typename T>
+__global__ void k_tvb_geo(int K, const double *V, T *tgeo) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= K) return;
   const double XV[3] = {V[e], V[K + e], V[2 * (size_t)K + e]};
@@ -93,22 +96,23 @@ __global__ void k_tvb_geo(int K, const double *V, double *tgeo) {
     const double dx = XV[(f + 1) % 3] - XV[f], dy = YV[(f + 1) % 3] - YV[f];
     len[f] = sqrt(dx * dx + dy * dy);
   }
-  tgeo[e] = (4.0 * A) / ((len[0] + len[1]) + len[2]);
+  tgeo[e] = (T)((4.0 * A) / ((len[0] + len[1]) + len[2]));
   const double bx = (XV[0] + XV[1] + XV[2]) / 3.0, by = (YV[0] + YV[1] + YV[2]) / 3.0;
   for (int i = 0; i < 3; i++) {
     const double mx = 0.5 * (XV[i] + XV[(i + 1) % 3]), my = 0.5 * (YV[i] + YV[(i + 1) % 3]);
     const double tx = mx - bx, ty = my - by;
     const double tl = sqrt(tx * tx + ty * ty);
-    tgeo[(size_t)(1 + 2 * i) * K + e] = tx / tl;
-    tgeo[(size_t)(2 + 2 * i) * K + e] = ty / tl;
+    tgeo[(size_t)(1 + 2 * i) * K + e] = (T)(tx / tl);
+    tgeo[(size_t)(2 + 2 * i) * K + e] = (T)(ty / tl);
   }
 }
 
-__global__ void k_scatter_field(int K, int Np, const int *orig, const double *src, double *dst) {
+template <typename T>
+__global__ void k_scatter_field(int K, int Np, const int *orig, const double *src, T *dst) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   size_t e = (size_t)orig[k];
-  for (int i = 0; i < Np; i++) dst[(size_t)i * K + k] = src[e * Np + i];
+  for (int i = 0; i < Np; i++) dst[(size_t)i * K + k] = (T)src[e * Np + i];
 }
 
 // internal committed state (parity per level) -> caller layout
@@ -116,25 +120,27 @@ struct GatherParams {
   int K, Np, nlev, off[9], par[8];  // K = elements to process (owned), Kstride = array stride
   int Kstride;
   const int *orig;
-  const double *Q;
+  const void *Q;  // T-typed internal state
   double *h, *hu, *hv;
 };
+template <typename T>
 __global__ void k_gather_state(const __grid_constant__ GatherParams p) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= p.K) return;
   int c = 0;
   for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
   const size_t K = p.Kstride;
-  const double *Q = p.Q + (size_t)p.par[c] * 3 * p.Np * K;
+  const T *Q = (const T *)p.Q + (size_t)p.par[c] * 3 * p.Np * K;
   size_t e = (size_t)p.orig[k];
   for (int i = 0; i < p.Np; i++) {
-    p.h[e * p.Np + i] = Q[(size_t)i * K + k];
-    p.hu[e * p.Np + i] = Q[(size_t)(p.Np + i) * K + k];
-    p.hv[e * p.Np + i] = Q[(size_t)(2 * p.Np + i) * K + k];
+    p.h[e * p.Np + i] = (double)Q[(size_t)i * K + k];
+    p.hu[e * p.Np + i] = (double)Q[(size_t)(p.Np + i) * K + k];
+    p.hv[e * p.Np + i] = (double)Q[(size_t)(2 * p.Np + i) * K + k];
   }
 }
 
 // mass and min h per block -> partials[2*block]
+template <typename T>
 __global__ void k_diag(const __grid_constant__ GatherParams p, const double *V, const double *wm2,
                        double *partials) {
   __shared__ double smass[256], smin[256];
@@ -144,12 +150,12 @@ __global__ void k_diag(const __grid_constant__ GatherParams p, const double *V, 
     int c = 0;
     for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
     const size_t K = p.Kstride;
-    const double *Q = p.Q + (size_t)p.par[c] * 3 * p.Np * K;
+    const T *Q = (const T *)p.Q + (size_t)p.par[c] * 3 * p.Np * K;
     double x0 = V[k], x1 = V[K + k], x2 = V[2 * K + k], y0 = V[3 * K + k], y1 = V[4 * K + k], y2 = V[5 * K + k];
     double J = 0.25 * ((x1 - x0) * (y2 - y0) - (x2 - x0) * (y1 - y0));
     double acc = 0.0;
     for (int i = 0; i < p.Np; i++) {
-      double h = Q[(size_t)i * K + k];
+      double h = (double)Q[(size_t)i * K + k];
       acc += wm2[i] * h;
       mn = fmin(mn, h);
     }
@@ -192,6 +198,8 @@ struct Ctx {
   int rank = 0, nranks = 1;
   double g = 9.81;
   swe_params prm;
+  bool f32 = false;  // FP32 variant (swe_params.precision == 32): T = float for the state and kernels
+  size_t esz = 8;    // bytes per element of the T-typed arrays
   cudaStream_t stream = 0;
   RefOps ops;
   HostMesh mesh;  // given mesh, with connectivity
@@ -205,7 +213,7 @@ struct Ctx {
   // device
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
   double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
-  double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dRmin = nullptr;
+  double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dOpsGf = nullptr, *dRmin = nullptr;
   double *dXsBuf = nullptr, *dXrBuf = nullptr;
   int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
   size_t xcap = 0;  // capacity (entries) of the exchange index/buffer arrays
@@ -280,34 +288,45 @@ static int cuda_fail(Ctx *c, cudaError_t e, const char *where) {
     }                                                                      \
   } while (0)
 
-template <int N>
-static cudaError_t upload_ops(const RefOps &o) {
-  Ops<N> h;
+template <int N, typename T>
+static void fill_ops(const RefOps &o, Ops<N, T> &h) {
   constexpr int Np = Ops<N>::Np, Nc = Ops<N>::Nc, Ng = Ops<N>::Ng, Nfp = Ops<N>::Nfp;
-  if (o.Nc != Nc || o.Np != Np) return cudaErrorInvalidValue;  // host rule and kernel template disagree
   for (int c = 0; c < Nc; c++)
     for (int i = 0; i < Np; i++) {
-      h.Ic[c][i] = o.Ic(c, i);
-      h.IcDr[c][i] = o.IcDr(c, i);
-      h.IcDs[c][i] = o.IcDs(c, i);
-      h.Pr[i][c] = o.Pr(i, c);
-      h.Ps[i][c] = o.Ps(i, c);
-      h.P[i][c] = o.P(i, c);
+      h.Ic[c][i] = (T)o.Ic(c, i);
+      h.IcDr[c][i] = (T)o.IcDr(c, i);
+      h.IcDs[c][i] = (T)o.IcDs(c, i);
+      h.Pr[i][c] = (T)o.Pr(i, c);
+      h.Ps[i][c] = (T)o.Ps(i, c);
+      h.P[i][c] = (T)o.P(i, c);
     }
   for (int i = 0; i < Np; i++)
-    for (int g = 0; g < 3 * Ng; g++) h.Lg[i][g] = o.Lg(i, g);
+    for (int g = 0; g < 3 * Ng; g++) h.Lg[i][g] = (T)o.Lg(i, g);
   for (int j = 0; j < Ng; j++)
-    for (int k = 0; k < Nfp; k++) h.Ig1[j][k] = o.Ig1(j, k);
+    for (int k = 0; k < Nfp; k++) h.Ig1[j][k] = (T)o.Ig1(j, k);
   for (int i = 0; i < Np; i++) {
-    h.wm2[i] = 0.5 * o.wmean[i];
-    for (int v = 0; v < 3; v++) h.Pv[v][i] = o.Pv(v, i);
-    h.lam[i][0] = -0.5 * (o.r[i] + o.s[i]);
-    h.lam[i][1] = 0.5 * (1.0 + o.r[i]);
-    h.lam[i][2] = 0.5 * (1.0 + o.s[i]);
+    h.wm2[i] = (T)(0.5 * o.wmean[i]);
+    for (int v = 0; v < 3; v++) h.Pv[v][i] = (T)o.Pv(v, i);
+    h.lam[i][0] = (T)(-0.5 * (o.r[i] + o.s[i]));
+    h.lam[i][1] = (T)(0.5 * (1.0 + o.r[i]));
+    h.lam[i][2] = (T)(0.5 * (1.0 + o.s[i]));
   }
+}
+
+template <int N>
+static cudaError_t upload_ops(const RefOps &o) {
+  if (o.Nc != Ops<N>::Nc || o.Np != Ops<N>::Np) return cudaErrorInvalidValue;  // host rule and kernel template disagree
+  Ops<N> h;
+  Ops<N, float> hf;
+  fill_ops<N, double>(o, h);
+  fill_ops<N, float>(o, hf);
   const void *sym = N == 1 ? (const void *)&c_ops1
                            : (N == 2 ? (const void *)&c_ops2 : (N == 3 ? (const void *)&c_ops3 : (const void *)&c_ops4));
-  return cudaMemcpyToSymbol(sym, &h, sizeof(h));
+  const void *symf = N == 1 ? (const void *)&c_opsf1
+                            : (N == 2 ? (const void *)&c_opsf2 : (N == 3 ? (const void *)&c_opsf3 : (const void *)&c_opsf4));
+  cudaError_t e = cudaMemcpyToSymbol(sym, &h, sizeof(h));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(symf, &hf, sizeof(hf));
 }
 
 template <int N>
@@ -370,11 +389,11 @@ static cudaError_t upload_ops_any(const RefOps &o) {
   return cudaErrorInvalidValue;
 }
 
-template <int N, bool INIT>
-static void launch_k1(const StepParams &p, cudaStream_t s) {
+template <int N, bool INIT, typename T>
+static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
-  size_t smem = INIT ? 0 : sizeof(double) * SmemOps<N>::scalar_total;
+  size_t smem = INIT ? 0 : sizeof(T) * SmemOps<N>::scalar_total;
   int grid = (n + K1_BLOCK - 1) / K1_BLOCK;
 #if K1_PERSIST
   static int resident = 0;  // one per template instance: SMs x resident blocks per SM
@@ -382,12 +401,12 @@ static void launch_k1(const StepParams &p, cudaStream_t s) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update<N, INIT>, K1_BLOCK, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update<N, INIT, T>, K1_BLOCK, smem);
     resident = std::max(1, sms * per_sm);
   }
   grid = std::min(grid, resident);
 #endif
-  if (!INIT && N >= K1_MMA_MIN_N) {
+  if constexpr (!INIT && N >= K1_MMA_MIN_N && sizeof(T) == 8) {  // FP64 tensor path (FP32: scalar path)
     const size_t smem_mma =
         sizeof(double) * (SmemOps<N>::total + (K1_MMA_TILE ? (size_t)(4 * SmemOps<N>::Np + 1) * (K1_BLOCK + kTilePad) : 0));
     static bool attr = false;
@@ -395,44 +414,77 @@ static void launch_k1(const StepParams &p, cudaStream_t s) {
       cudaFuncSetAttribute(k_rhs_update_mma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mma);
       attr = true;
     }
-    k_rhs_update_mma<N><<<(n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem_mma, s>>>(p);
+    k_rhs_update_mma<N><<<(n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem_mma, s>>>(
+        reinterpret_cast<const StepParams &>(p));
     return;
   }
-  k_rhs_update<N, INIT><<<grid, K1_BLOCK, smem, s>>>(p);
+  k_rhs_update<N, INIT, T><<<grid, K1_BLOCK, smem, s>>>(p);
 }
-template <int N>
-static void launch_k2(const StepParams &p, cudaStream_t s) {
+template <int N, typename T>
+static void launch_k2(const StepParamsT<T> &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
-  k_tvb<N><<<(n + 127) / 128, 128, 0, s>>>(p);
+  k_tvb<N, T><<<(n + 127) / 128, 128, 0, s>>>(p);
 }
-static void launch(int which, bool init, int N, const StepParams &p, cudaStream_t s) {
+template <typename T>
+static void launch_t(int which, bool init, int N, const StepParamsT<T> &p, cudaStream_t s) {
   if (which == 0) {
     switch (N) {
-      case 1: init ? launch_k1<1, true>(p, s) : launch_k1<1, false>(p, s); break;
-      case 2: init ? launch_k1<2, true>(p, s) : launch_k1<2, false>(p, s); break;
-      case 3: init ? launch_k1<3, true>(p, s) : launch_k1<3, false>(p, s); break;
-      case 4: init ? launch_k1<4, true>(p, s) : launch_k1<4, false>(p, s); break;
+      case 1: init ? launch_k1<1, true, T>(p, s) : launch_k1<1, false, T>(p, s); break;
+      case 2: init ? launch_k1<2, true, T>(p, s) : launch_k1<2, false, T>(p, s); break;
+      case 3: init ? launch_k1<3, true, T>(p, s) : launch_k1<3, false, T>(p, s); break;
+      case 4: init ? launch_k1<4, true, T>(p, s) : launch_k1<4, false, T>(p, s); break;
     }
   } else {
     switch (N) {
-      case 1: launch_k2<1>(p, s); break;
-      case 2: launch_k2<2>(p, s); break;
-      case 3: launch_k2<3>(p, s); break;
-      case 4: launch_k2<4>(p, s); break;
+      case 1: launch_k2<1, T>(p, s); break;
+      case 2: launch_k2<2, T>(p, s); break;
+      case 3: launch_k2<3, T>(p, s); break;
+      case 4: launch_k2<4, T>(p, s); break;
     }
   }
 }
 
+// The host builds every update's parameters in double; the FP32 variant gets a
+// copy with float scalars and its float-typed device arrays.
+static StepParamsT<float> to_f32(const StepParams &d) {
+  StepParamsT<float> f;
+  std::memset(&f, 0, sizeof(f));
+  f.k0 = d.k0, f.k1 = d.k1, f.K = d.K;
+  f.Q = (float *)d.Q, f.R = (float *)d.R, f.B = (const float *)d.B, f.V = d.V, f.E2E = d.E2E, f.tcode = d.tcode;
+  f.talpha = (const float *)d.talpha, f.geo = (const float *)d.geo, f.tgeo = (const float *)d.tgeo;
+  f.means = (float *)d.means, f.dry = d.dry, f.UT = (float *)d.UT;
+  f.own_par = d.own_par, f.write_par = d.write_par, f.write_slot = d.write_slot, f.nab = d.nab;
+  for (int i = 0; i < 3; i++) f.ab_slot[i] = d.ab_slot[i], f.ab[i] = (float)d.ab[i];
+  f.nlev = d.nlev, f.kown = d.kown;
+  for (int l = 0; l <= 8; l++) f.off[l] = d.off[l], f.goff[l] = d.goff[l];
+  for (int l = 0; l < 8; l++) {
+    f.lev[l].par = d.lev[l].par, f.lev[l].dense = d.lev[l].dense, f.lev[l].nterm = d.lev[l].nterm;
+    for (int s = 0; s < 3; s++) f.lev[l].slot[s] = d.lev[l].slot[s], f.lev[l].beta[s] = (float)d.lev[l].beta[s];
+  }
+  f.g = (float)d.g, f.h0 = (float)d.h0, f.eps = (float)d.eps, f.e4 = (float)d.e4;
+  f.tvb_M = (float)d.tvb_M, f.tvb_nu = (float)d.tvb_nu, f.h_char = (float)d.h_char;
+  f.use_pp = d.use_pp, f.use_tvb = d.use_tvb;
+  f.counters = d.counters, f.injected = d.injected, f.opsG = (const float *)d.opsG;
+  return f;
+}
+
+static void launch(int which, bool init, int N, const StepParams &p, cudaStream_t s, bool f32) {
+  if (f32)
+    launch_t<float>(which, init, N, to_f32(p), s);
+  else
+    launch_t<double>(which, init, N, p, s);
+}
+
 // algorithmic bytes per element update
-static double k1_bytes(int N, int nab, bool tvb) {
+static double k1_bytes(int N, int nab, bool tvb, size_t esz) {
   int Np = (N + 1) * (N + 2) / 2, Nfp = N + 1;
   double d = 3 * Np /*Q r*/ + 3 * Np /*Q w*/ + 3 * Np /*R w*/ + 3 * Np * (nab - 1) /*R r*/ + Np /*B*/ +
              9 * Nfp /*nbr Q faces*/ + 3 * Nfp /*nbr B faces*/ + 14 /*geometry table*/ + 3 /*means w*/ + (tvb ? 9 : 0);
-  return 8.0 * d + 12.0 /*E2E*/ + 1.0 /*dry flag*/;
+  return (double)esz * d + 12.0 /*E2E*/ + 1.0 /*dry flag*/;
 }
 // own means, 3 neighbours' means, P1 midpoint data, alphas, static geometry (tgeo); E2E, pair code, 4 dry flags
-static double k2_bytes() { return 8.0 * (3 + 9 + 9 + 6 + 7) + 12.0 + 4.0 + 4.0; }
+static double k2_bytes(size_t esz) { return (double)esz * (3 + 9 + 9 + 6 + 7) + 12.0 + 4.0 + 4.0; }
 
 static StepParams base_params(Ctx *c) {
   StepParams p;
@@ -462,7 +514,7 @@ static StepParams base_params(Ctx *c) {
   p.use_tvb = c->prm.use_tvb;
   p.counters = c->dCounters;
   p.injected = c->dInjected;
-  p.opsG = c->dOpsG;
+  p.opsG = c->f32 ? c->dOpsGf : c->dOpsG;
   p.nlev = c->L;
   p.kown = c->kown;
   for (int l = 0; l <= 8; l++) {
@@ -475,15 +527,16 @@ static StepParams base_params(Ctx *c) {
 static int alloc_state(Ctx *c) {
   if (c->dQ) return SWE_OK;
   size_t K = c->K, Np = c->Np, Kin = c->Kin;
-  c->dQ = (double *)c->dalloc(sizeof(double) * 2 * 3 * Np * K);
-  c->dR = (double *)c->dalloc(sizeof(double) * 3 * 3 * Np * K);
-  c->dB = (double *)c->dalloc(sizeof(double) * Np * K);
+  const size_t es = c->esz;  // T-typed arrays
+  c->dQ = (double *)c->dalloc(es * 2 * 3 * Np * K);
+  c->dR = (double *)c->dalloc(es * 3 * 3 * Np * K);
+  c->dB = (double *)c->dalloc(es * Np * K);
   c->dV = (double *)c->dalloc(sizeof(double) * 6 * K);
-  c->dMeans = (double *)c->dalloc(sizeof(double) * 3 * K);
-  c->dUT = (double *)c->dalloc(sizeof(double) * 9 * K);
-  c->dTalpha = (double *)c->dalloc(sizeof(double) * 6 * K);
-  c->dTgeo = (double *)c->dalloc(sizeof(double) * 7 * K);
-  c->dGeo = (double *)c->dalloc(sizeof(double) * 14 * K);
+  c->dMeans = (double *)c->dalloc(es * 3 * K);
+  c->dUT = (double *)c->dalloc(es * 9 * K);
+  c->dTalpha = (double *)c->dalloc(es * 6 * K);
+  c->dTgeo = (double *)c->dalloc(es * 7 * K);
+  c->dGeo = (double *)c->dalloc(es * 14 * K);
   c->dAe = (double *)c->dalloc(sizeof(double) * Kin);
   c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * Kin);
   c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
@@ -498,8 +551,8 @@ static int alloc_state(Ctx *c) {
   c->xcap = std::max(ns, nr) + 1;
   c->dXsIdx = (int *)c->dalloc(sizeof(int) * c->xcap);
   c->dXrIdx = (int *)c->dalloc(sizeof(int) * c->xcap);
-  c->dXsBuf = (double *)c->dalloc(sizeof(double) * 6 * Np * c->xcap);
-  c->dXrBuf = (double *)c->dalloc(sizeof(double) * 6 * Np * c->xcap);
+  c->dXsBuf = (double *)c->dalloc(es * 6 * Np * c->xcap);
+  c->dXrBuf = (double *)c->dalloc(es * 6 * Np * c->xcap);
   if (!c->alloc_ok) {
     c->err = "device allocation failed";
     return SWE_ERR_NOMEM;
@@ -536,21 +589,28 @@ static int xpack(Ctx *c, int phase, int lvl, int par, int slot) {
   if (c->plan.peers.empty()) return SWE_OK;
   int a = lvl == 0 ? 0 : c->xs.loff[lvl - 1], b = lvl == 0 ? c->xs.total : c->xs.loff[lvl];
   if (b <= a) return SWE_OK;
-  HaloParams h;
-  std::memset(&h, 0, sizeof(h));
-  h.n = b - a;
-  h.K = c->K;
-  h.Np = c->Np;
-  h.phase = phase;
-  h.par = par;
-  h.slot = slot;
-  h.idx = c->dXsIdx + a;
-  h.buf = c->dXsBuf + (size_t)payload(c, phase) * a;
-  h.Q = c->dQ;
-  h.R = c->dR;
-  h.means = c->dMeans;
-  h.dry = c->dDry;
-  k_halo_pack<<<(h.n + 127) / 128, 128, 0, c->stream>>>(h);
+  auto run = [&](auto tag) {
+    using T = decltype(tag);
+    HaloParamsT<T> h;
+    std::memset(&h, 0, sizeof(h));
+    h.n = b - a;
+    h.K = c->K;
+    h.Np = c->Np;
+    h.phase = phase;
+    h.par = par;
+    h.slot = slot;
+    h.idx = c->dXsIdx + a;
+    h.buf = (T *)c->dXsBuf + (size_t)payload(c, phase) * a;
+    h.Q = (T *)c->dQ;
+    h.R = (T *)c->dR;
+    h.means = (T *)c->dMeans;
+    h.dry = c->dDry;
+    k_halo_pack<T><<<(h.n + 127) / 128, 128, 0, c->stream>>>(h);
+  };
+  if (c->f32)
+    run(float{});
+  else
+    run(double{});
   CK(cudaGetLastError());
   return SWE_OK;
 }
@@ -559,21 +619,28 @@ static int xunpack(Ctx *c, int phase, int lvl, int par, int slot) {
   if (c->plan.peers.empty()) return SWE_OK;
   int a = lvl == 0 ? 0 : c->xr.loff[lvl - 1], b = lvl == 0 ? c->xr.total : c->xr.loff[lvl];
   if (b <= a) return SWE_OK;
-  HaloParams h;
-  std::memset(&h, 0, sizeof(h));
-  h.n = b - a;
-  h.K = c->K;
-  h.Np = c->Np;
-  h.phase = phase;
-  h.par = par;
-  h.slot = slot;
-  h.idx = c->dXrIdx + a;
-  h.buf = c->dXrBuf + (size_t)payload(c, phase) * a;
-  h.Q = c->dQ;
-  h.R = c->dR;
-  h.means = c->dMeans;
-  h.dry = c->dDry;
-  k_halo_unpack<<<(h.n + 127) / 128, 128, 0, c->stream>>>(h);
+  auto run = [&](auto tag) {
+    using T = decltype(tag);
+    HaloParamsT<T> h;
+    std::memset(&h, 0, sizeof(h));
+    h.n = b - a;
+    h.K = c->K;
+    h.Np = c->Np;
+    h.phase = phase;
+    h.par = par;
+    h.slot = slot;
+    h.idx = c->dXrIdx + a;
+    h.buf = (T *)c->dXrBuf + (size_t)payload(c, phase) * a;
+    h.Q = (T *)c->dQ;
+    h.R = (T *)c->dR;
+    h.means = (T *)c->dMeans;
+    h.dry = c->dDry;
+    k_halo_unpack<T><<<(h.n + 127) / 128, 128, 0, c->stream>>>(h);
+  };
+  if (c->f32)
+    run(float{});
+  else
+    run(double{});
   CK(cudaGetLastError());
   return SWE_OK;
 }
@@ -589,8 +656,10 @@ static int xtransfer(Ctx *c, int phase, int lvl) {
       for (int l = (lvl == 0 ? 1 : lvl); l <= (lvl == 0 ? c->L : lvl); l++) {
         int so = c->xs.off[(size_t)l * np + i], sc = c->xs.cnt[(size_t)l * np + i];
         int ro = c->xr.off[(size_t)l * np + i], rc = c->xr.cnt[(size_t)l * np + i];
-        if (sc > 0) NK(ncclSend(c->dXsBuf + (size_t)P * so, (size_t)P * sc, ncclDouble, c->plan.peers[i], c->comm, c->stream));
-        if (rc > 0) NK(ncclRecv(c->dXrBuf + (size_t)P * ro, (size_t)P * rc, ncclDouble, c->plan.peers[i], c->comm, c->stream));
+        const ncclDataType_t dt = c->f32 ? ncclFloat : ncclDouble;
+        char *sb = (char *)c->dXsBuf, *rb = (char *)c->dXrBuf;
+        if (sc > 0) NK(ncclSend(sb + c->esz * P * so, (size_t)P * sc, dt, c->plan.peers[i], c->comm, c->stream));
+        if (rc > 0) NK(ncclRecv(rb + c->esz * P * ro, (size_t)P * rc, dt, c->plan.peers[i], c->comm, c->stream));
       }
     }
     NK(ncclGroupEnd());
@@ -615,7 +684,7 @@ static int xtransfer(Ctx *c, int phase, int lvl) {
           return SWE_ERR_STATE;
         }
         if (rc > 0)
-          CK(cudaMemcpyAsync(c->dXrBuf + (size_t)P * ro, q->dXsBuf + (size_t)P * so, sizeof(double) * P * rc,
+          CK(cudaMemcpyAsync((char *)c->dXrBuf + c->esz * P * ro, (char *)q->dXsBuf + c->esz * P * so, c->esz * P * rc,
                              cudaMemcpyDeviceToDevice, c->stream));
       }
     }
@@ -719,7 +788,13 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   build_xtable(c, c->plan.send, inv, c->xs, xsf);
   build_xtable(c, c->plan.recv, inv, c->xr, xrf);
   CK(cudaMemcpyAsync(c->dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->dTalpha, TA.data(), sizeof(double) * TA.size(), cudaMemcpyHostToDevice, c->stream));
+  std::vector<float> TAf;
+  if (c->f32) {
+    TAf.assign(TA.begin(), TA.end());
+    CK(cudaMemcpyAsync(c->dTalpha, TAf.data(), sizeof(float) * TAf.size(), cudaMemcpyHostToDevice, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(c->dTalpha, TA.data(), sizeof(double) * TA.size(), cudaMemcpyHostToDevice, c->stream));
+  }
   CK(cudaMemcpyAsync(c->dE2E, E2E.data(), sizeof(int) * E2E.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dTcode, TC.data(), sizeof(int) * TC.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dOrig, c->order.data(), sizeof(int) * K, cudaMemcpyHostToDevice, c->stream));
@@ -729,9 +804,15 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
     CK(cudaMemcpyAsync(c->dXrIdx, xrf.data(), sizeof(int) * xrf.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));  // host vectors above are released on return
   int nb = (K + 127) / 128;
-  k_scatter_field<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dBcaller, c->dB);
-  k_tvb_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dTgeo);
-  k_geo<<<nb, 128, 0, c->stream>>>(K, c->dV, c->dGeo);
+  if (c->f32) {
+    k_scatter_field<float><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dBcaller, (float *)c->dB);
+    k_tvb_geo<float><<<nb, 128, 0, c->stream>>>(K, c->dV, (float *)c->dTgeo);
+    k_geo<float><<<nb, 128, 0, c->stream>>>(K, c->dV, (float *)c->dGeo);
+  } else {
+    k_scatter_field<double><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dBcaller, c->dB);
+    k_tvb_geo<double><<<nb, 128, 0, c->stream>>>(K, c->dV, c->dTgeo);
+    k_geo<double><<<nb, 128, 0, c->stream>>>(K, c->dV, c->dGeo);
+  }
   CK(cudaGetLastError());
   c->layout_valid = true;
   return materialize_state(c);
@@ -743,8 +824,12 @@ static int materialize_state(Ctx *c) {
   const int K = c->K;
   const int nb = (K + 127) / 128;
   const size_t KNp = (size_t)c->Kin * c->Np;
-  k_scatter_state<<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp, c->dStage + 2 * KNp,
-                                             c->dQ);
+  if (c->f32)
+    k_scatter_state<float><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp,
+                                                      c->dStage + 2 * KNp, (float *)c->dQ);
+  else
+    k_scatter_state<double><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp,
+                                                       c->dStage + 2 * KNp, c->dQ);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
   CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
@@ -853,14 +938,14 @@ static void launch_timed(Ctx *c, int which, const StepParams &p) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, c->stream);
-    launch(which, false, c->N, p, c->stream);
+    launch(which, false, c->N, p, c->stream, c->f32);
     cudaEventRecord(e1, c->stream);
     c->ev.push_back(e0);
     c->ev.push_back(e1);
-    c->prof_bytes[which] += (which == 0 ? k1_bytes(c->N, p.nab, c->prm.use_tvb) : k2_bytes()) * nel;
+    c->prof_bytes[which] += (which == 0 ? k1_bytes(c->N, p.nab, c->prm.use_tvb, c->esz) : k2_bytes(c->esz)) * nel;
     c->prof_launch[which]++;
   } else {
-    launch(which, false, c->N, p, c->stream);
+    launch(which, false, c->N, p, c->stream, c->f32);
   }
 }
 
@@ -916,7 +1001,7 @@ static int group_init_limit(std::vector<Ctx *> &G) {
     p.own_par = 0;
     p.write_par = 0;
     c->cur = p;
-    launch(0, true, c->N, p, c->stream);
+    launch(0, true, c->N, p, c->stream, c->f32);
     CK(cudaGetLastError());
   }
   for (Ctx *c : G)
@@ -926,7 +1011,7 @@ static int group_init_limit(std::vector<Ctx *> &G) {
   for (Ctx *c : G)
     if (int rc = xunpack(c, 0, 0, 0, 0)) return rc;
   for (Ctx *c : G)
-    if (c->prm.use_tvb) launch(1, false, c->N, c->cur, c->stream);
+    if (c->prm.use_tvb) launch(1, false, c->N, c->cur, c->stream, c->f32);
   for (Ctx *c : G)
     if (int rc = xpack(c, 1, 0, 0, -1)) return rc;
   for (Ctx *c : G)
@@ -1129,6 +1214,12 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
     swe_destroy(h);
     return rc;
   };
+  if (c->prm.precision != 0 && c->prm.precision != 32 && c->prm.precision != 64) {
+    c->err = "precision must be 32 or 64";
+    return fail(SWE_ERR_ARG);
+  }
+  c->f32 = c->prm.precision == 32;
+  c->esz = c->f32 ? sizeof(float) : sizeof(double);
   if (c->rank < 0 || c->rank >= c->nranks) return fail(SWE_ERR_ARG);
   int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, c->mesh, &c->err);
   if (rc) return fail(rc);
@@ -1174,6 +1265,8 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   c->dWm2 = (double *)c->dalloc(sizeof(double) * c->Np);
   std::vector<double> sops = smem_ops_any(c->ops);
   c->dOpsG = (double *)c->dalloc(sizeof(double) * sops.size());
+  std::vector<float> sopsf(sops.begin(), sops.end());
+  c->dOpsGf = (double *)c->dalloc(sizeof(float) * sopsf.size());
   c->dCounters = (unsigned long long *)c->dalloc(sizeof(unsigned long long) * 4 * kSlots);
   c->dInjected = (double *)c->dalloc(sizeof(double) * kSlots);
   if (!c->alloc_ok) return fail(SWE_ERR_NOMEM);
@@ -1185,6 +1278,8 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
           cudaSuccess ||
       cudaMemcpyAsync(c->dWm2, wm2.data(), sizeof(double) * c->Np, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
       cudaMemcpyAsync(c->dOpsG, sops.data(), sizeof(double) * sops.size(), cudaMemcpyHostToDevice, c->stream) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(c->dOpsGf, sopsf.data(), sizeof(float) * sopsf.size(), cudaMemcpyHostToDevice, c->stream) !=
           cudaSuccess ||
       cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream) != cudaSuccess ||
@@ -1275,7 +1370,10 @@ int swe_get_state(swe_ctx *h, double *hh, double *hu, double *hv) {
   double *tmp = (double *)c->dalloc(sizeof(double) * 3 * KNp);
   if (!tmp) return SWE_ERR_NOMEM;
   GatherParams g = gather_params(c, tmp, tmp + KNp, tmp + 2 * KNp);
-  k_gather_state<<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
+  if (c->f32)
+    k_gather_state<float><<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
+  else
+    k_gather_state<double><<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
   cudaError_t e = cudaGetLastError();
   if (c->kown == c->Kin) {  // every element owned: straight copies
     if (e == cudaSuccess) e = cudaMemcpyAsync(hh, tmp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
@@ -1313,7 +1411,7 @@ void swe_destroy(swe_ctx *h) {
         if (p == c) p = nullptr;
     }
   void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo,
-                  c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG,
+                  c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG, c->dOpsGf,
                   c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
                   c->dXrIdx,   c->dDry,   c->dCounters};
   for (void *p : ptrs) c->dfree(p);
@@ -1358,7 +1456,10 @@ int swe_get_info(swe_ctx *h, swe_info *info) {
   if (rc) return rc;
   int nb = (c->kown + 255) / 256;
   GatherParams g = gather_params(c, nullptr, nullptr, nullptr);
-  k_diag<<<nb, 256, 0, c->stream>>>(g, c->dV, c->dWm2, c->dPartials);
+  if (c->f32)
+    k_diag<float><<<nb, 256, 0, c->stream>>>(g, c->dV, c->dWm2, c->dPartials);
+  else
+    k_diag<double><<<nb, 256, 0, c->stream>>>(g, c->dV, c->dWm2, c->dPartials);
   std::vector<double> part(2 * (size_t)nb);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(part.data(), c->dPartials, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, c->stream));
