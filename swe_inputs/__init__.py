@@ -249,6 +249,112 @@ def c4_dambreak(N: int = 3, base: int = 1, shuffle_seed: int | None = SEED) -> W
     return Workload("C4", m, N, 9.81, B, init, prm, 3, 0.2, 100)
 
 
+def annulus(nr: int, nth: int, r0: float, r1: float) -> Mesh:
+    """Polar grid of the annulus r0 <= r <= r1 (nr rings, nth sectors), each cell split into two
+    counter-clockwise triangles; the seam at theta = 0 closes through shared vertices."""
+    rs = r0 + (r1 - r0) / nr * np.arange(nr + 1)
+    th = 2.0 * math.pi / nth * np.arange(nth)
+    R, TH = np.meshgrid(rs, th, indexing="ij")  # vertex (i, j) -> i * nth + j
+    vx, vy = (R * np.cos(TH)).ravel().copy(), (R * np.sin(TH)).ravel().copy()
+    vid = lambda i, j: i * nth + (j % nth)  # noqa: E731
+    i, j = np.meshgrid(np.arange(nr), np.arange(nth), indexing="ij")
+    i, j = i.ravel(), j.ravel()
+    a, b, c, d = vid(i, j), vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)
+    etov = np.empty((2 * nr * nth, 3), dtype=np.int32)
+    etov[0::2] = np.stack([a, b, c], 1)  # (r, th) -> (r+, th) -> (r+, th+): counter-clockwise
+    etov[1::2] = np.stack([a, c, d], 1)
+    return Mesh(vx, vy, etov, None)
+
+
+COUETTE = dict(r0=2.0, r1=4.0, g=1.0)
+
+
+def couette_exact():
+    """Couette flow between concentric cylinders: h = 1, u_theta = (-r + 16/r)/75,
+    B = (r^2/2 - 32 log r - 128/r^2)/75^2; steady.  g = 1 (reading A27: forced by the balance
+    u_theta^2 / r = g dB/dr); annulus 2 <= r <= 4 (reading A28)."""
+    def B(x, y):
+        r2 = x * x + y * y
+        return (0.5 * r2 - 16.0 * np.log(r2) - 128.0 / r2) / 75.0 ** 2
+
+    def ex(x, y, t):
+        r = np.sqrt(x * x + y * y)
+        ut = (-r + 16.0 / r) / 75.0
+        h = np.ones_like(x)
+        return h, -h * ut * y / r, h * ut * x / r
+    return B, ex
+
+
+def c6_couette(N: int = 2, nr: int = 4, nth: int = 24, shuffle_seed: int | None = SEED) -> Workload:
+    """Couette flow on the annulus 2 <= r <= 4 (walls = the two cylinders, straight-sided),
+    smooth steady state, no limiters."""
+    m = annulus(nr, nth, COUETTE["r0"], COUETTE["r1"])
+    if shuffle_seed is not None:
+        m = shuffle(m, shuffle_seed)
+    B, ex = couette_exact()
+    prm = dict(h0=1e-8, use_pp=0, use_tvb=0)
+    return Workload(f"Couette-{nr}x{nth}", m, N, COUETTE["g"], B, lambda x, y: ex(x, y, 0.0), prm, 1, 0.2, 0, ex)
+
+
+def rarefaction_exact(h0: float = 1.0, g: float = 1.0, x0: float = 20.0):
+    """Dam break into a dry bed: xi = (x - 20)/t; h = h0 left of -sqrt(g h0),
+    0 right of 2 sqrt(g h0), (xi - 2 sqrt(g h0))^2 / (9 g) between; u = 2/3 (xi + sqrt(g h0))."""
+    c0 = math.sqrt(g * h0)
+
+    def ex(x, y, t):
+        xi = (x - x0) / t
+        h = np.where(xi < -c0, h0, np.where(xi > 2 * c0, 0.0, (xi - 2 * c0) ** 2 / (9 * g)))
+        u = np.where(xi < -c0, 0.0, np.where(xi > 2 * c0, 0.0, 2.0 / 3.0 * (xi + c0)))
+        return h, h * u, np.zeros_like(x)
+    return ex
+
+
+def c7_rarefaction(N: int = 2, n: int = 1, t0: float = 2.0, shuffle_seed: int | None = SEED) -> Workload:
+    """Rarefaction wave on the flat 50 m x 40 m box, g = 1, h0 = 1: initial state =
+    the exact solution at t0 = 2 s (C0); PP limiter on, TVB off.  Walls: the wave stays
+    inside x in [20 - t, 20 + 2t] for t <= 15.  Mesh: 2 x (10 n) x (8 n) triangles (H = 5/n)."""
+    m = structured(10 * n, 8 * n, 0.0, 50.0, 0.0, 40.0)
+    if shuffle_seed is not None:
+        m = shuffle(m, shuffle_seed)
+    ex = rarefaction_exact()
+    prm = dict(h0=1e-6, use_pp=1, use_tvb=0)
+    w = Workload(f"Rarefaction-n{n}", m, N, 1.0, lambda x, y: np.zeros_like(x), lambda x, y: ex(x, y, t0), prm,
+                 1, 0.2, 0, ex)
+    w.t0 = t0
+    return w
+
+
+LAKE = dict(a=1.0, sigma=0.5, h0=0.1, g=9.81)
+
+
+def lake_exact(a=LAKE["a"], sigma=LAKE["sigma"], h0=LAKE["h0"], g=LAKE["g"]):
+    """Oscillating lake in a parabolic bowl (Eq. lake2d): B = h0 (x^2+y^2)/a^2,
+    h = max(0, sigma h0/a^2 (2x cos wt + 2y sin wt - sigma) + h0 - B), u = -sigma w sin wt,
+    v = sigma w cos wt, w = sqrt(2 g h0)/a."""
+    om = math.sqrt(2 * g * h0) / a
+
+    def B(x, y):
+        return h0 * (x * x + y * y) / a ** 2
+
+    def ex(x, y, t):
+        h = np.maximum(0.0, sigma * h0 / a ** 2 * (2 * x * math.cos(om * t) + 2 * y * math.sin(om * t) - sigma)
+                       + h0 - B(x, y))
+        return h, h * (-sigma * om * math.sin(om * t)), h * (sigma * om * math.cos(om * t))
+    return B, ex, om
+
+
+def c8_oscillating_lake(N: int = 2, n: int = 16, shuffle_seed: int | None = SEED) -> Workload:
+    """Oscillating lake on [-2,2]^2 with reflecting walls, PP + TVB.  H = 4/n."""
+    m = structured(n, n, -2.0, 2.0, -2.0, 2.0)
+    if shuffle_seed is not None:
+        m = shuffle(m, shuffle_seed)
+    B, ex, om = lake_exact()
+    prm = dict(h0=1e-6, tvb_M=1.0, tvb_nu=1.5, use_pp=1, use_tvb=1)
+    w = Workload(f"OscLake-n{n}", m, N, LAKE["g"], B, lambda x, y: ex(x, y, 0.0), prm, 1, 0.2, 0, ex)
+    w.period = 2 * math.pi / om
+    return w
+
+
 C5_LX = 2.0e6
 
 

@@ -1,0 +1,157 @@
+"""The paper's remaining verification workloads on the oracle, pinned to
+their exact solutions and to the invariants the paper and the mathematics fix.
+
+* Couette flow: the exact state balances the equations (g = 1, reading A27); the
+  oracle converges to it on refined annulus meshes.  The cylinders are straight-sided polygons
+  (reading A28), whose O(H) wall-normal error bounds the order, so the pin is a rate above 1.2
+  rather than the paper's N + 1/2.
+* Rarefaction wave into a dry bed: positivity at every node; the error in the smooth
+  part of the fan converges at least at the rate the paper reports for the projected solution
+  ("global error ... O(H^{1+1/2})", local O(H^{2.2}) / O(H^{3.0})), with margin for the
+  shorter run used here.
+* Oscillating lake: positivity; mass conserved up to the mass the dry branch of
+  Alg. 3 injects (reading A13); convergence to the exact planar solution inside the wet disc.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import swe_inputs as si
+from tests.common import make_oracle
+
+
+def _run(w, t_end, t0=0.0, u_max=0.0, h_max=1.0):
+    o, d = make_oracle(w)
+    o.set_state(d["h"], d["hu"], d["hv"])
+    dt = si.dt_for(w.mesh, w.N, w.g, h_max, 0.0, 0.2, u_max=u_max)
+    n = int(math.ceil((t_end - t0) / dt))
+    for _ in range(n):
+        assert o.step((t_end - t0) / n, 1) == 0
+    return o, d
+
+
+def _l2(o, w, t, field=0, region=None):
+    """L2 error against the exact solution with the nodal mass weights (exact for P^N)."""
+    x, y = o.nodes()
+    ex = w.exact(x, y, t)[field]
+    q = o.get_state()[field]
+    v = w.mesh.etov
+    X, Y = w.mesh.vx[v], w.mesh.vy[v]
+    A = 0.5 * np.abs((X[:, 1] - X[:, 0]) * (Y[:, 2] - Y[:, 0]) - (X[:, 2] - X[:, 0]) * (Y[:, 1] - Y[:, 0]))
+    wts = (A / 2.0)[:, None] * oracle.refel(w.N)["wmean"][None, :]
+    sel = np.ones_like(x, dtype=bool) if region is None else region(x, y)
+    return math.sqrt(float((wts * (q - ex) ** 2 * sel).sum()))
+
+
+# ------------------------------------------------------------------ Couette
+def test_couette_exact_balances_the_equations():
+    """u_theta^2 / r = g dB/dr with g = 1 (reading A27), checked through the momentum residual of
+    the steady SWE, u.grad(u) + g grad(h + B) = 0 (h = 1), by central differences."""
+    B, ex = si.couette_exact()
+    rng = np.random.default_rng(7)
+    r = rng.uniform(2.2, 3.8, 50)
+    th = rng.uniform(0, 2 * np.pi, 50)
+    x, y = r * np.cos(th), r * np.sin(th)
+    e = 1e-5
+
+    def vel(x, y):
+        h, hu, hv = ex(x, y, 0.0)
+        return hu / h, hv / h
+
+    u, v = vel(x, y)
+    ux = (vel(x + e, y)[0] - vel(x - e, y)[0]) / (2 * e)
+    uy = (vel(x, y + e)[0] - vel(x, y - e)[0]) / (2 * e)
+    vx = (vel(x + e, y)[1] - vel(x - e, y)[1]) / (2 * e)
+    vy = (vel(x, y + e)[1] - vel(x, y - e)[1]) / (2 * e)
+    Bx = (B(x + e, y) - B(x - e, y)) / (2 * e)
+    By = (B(x, y + e) - B(x, y - e)) / (2 * e)
+    g = si.COUETTE["g"]
+    assert np.abs(u * ux + v * uy + g * Bx).max() < 1e-9
+    assert np.abs(u * vx + v * vy + g * By).max() < 1e-9
+    assert np.abs(ux + vy).max() < 1e-9  # divergence-free, so h = 1 is steady
+    # with g = 9.81 the state is not steady (why A27 reads g = 1)
+    assert np.abs(u * ux + v * uy + 9.81 * Bx).max() > 1e-4
+
+
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_oracle_couette_converges(N):
+    errs = []
+    for nr, nth in [(2, 12), (4, 24), (8, 48)]:
+        w = si.c6_couette(N, nr, nth)
+        o, _ = _run(w, 1.0, u_max=0.1)
+        errs.append(_l2(o, w, 1.0, 0))
+    rates = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert errs[2] < errs[1] < errs[0]
+    assert min(rates) > 1.2, rates
+
+
+# ------------------------------------------------------------------ rarefaction
+def test_rarefaction_exact_is_continuous():
+    ex = si.rarefaction_exact()
+    c0 = 1.0
+    for t in (2.0, 5.0):
+        for xi in (-c0, 2 * c0):
+            x = 20.0 + xi * t
+            lo = ex(np.array([x - 1e-9]), np.zeros(1), t)
+            hi = ex(np.array([x + 1e-9]), np.zeros(1), t)
+            for a, b in zip(lo, hi):
+                assert abs(a[0] - b[0]) < 1e-8
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_oracle_rarefaction_positivity_and_accuracy(N):
+    """From the exact state at t = 2 s to t = 3 s (fan x in [17, 26]): every nodal depth stays
+    >= 0 (Alg. 3); the error converges globally and faster inside the smooth fan."""
+    glob, loc = [], []
+    for n in (2, 4, 8):
+        w = si.c7_rarefaction(N, n)
+        o, _ = _run(w, 3.0, t0=2.0, u_max=2.0)
+        assert o.get_state()[0].min() >= 0.0
+        assert o.info()["n_pp"] > 0
+        glob.append(_l2(o, w, 3.0))
+        loc.append(_l2(o, w, 3.0, region=lambda x, y: (x > 18.0) & (x < 24.0)))
+    assert glob[2] < glob[1] < glob[0] and loc[2] < loc[1] < loc[0]
+    assert math.log2(glob[1] / glob[2]) > 1.0
+    assert math.log2(loc[1] / loc[2]) > 1.8
+
+
+# ------------------------------------------------------------------ oscillating lake
+def test_lake_exact_vanishes_continuously_at_the_front():
+    B, ex, om = si.lake_exact()
+    for t in (0.0, 0.3, 1.1):
+        ang = np.linspace(0, 2 * np.pi, 64)
+        # the wet region is a disc of radius 1 centred at sigma (cos wt, sin wt) (a = 1)
+        cx, cy = si.LAKE["sigma"] * math.cos(om * t), si.LAKE["sigma"] * math.sin(om * t)
+        for rr, wet in ((1.0 - 1e-6, True), (1.0 + 1e-6, False)):
+            h = ex(cx + rr * np.cos(ang), cy + rr * np.sin(ang), t)[0]
+            assert np.abs(h).max() < 1e-6
+            assert (h > 0).all() if wet else (h == 0).all()
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_oracle_oscillating_lake(N):
+    errs = []
+    for n in (8, 16, 32):
+        w = si.c8_oscillating_lake(N, n)
+        o, d = _run(w, 0.1, u_max=0.5, h_max=0.2)
+        st = o.get_state()
+        assert st[0].min() >= 0.0
+        errs.append(_l2(o, w, 0.1, region=lambda x, y: (x - 0.5) ** 2 + y * y < 0.5))
+    assert errs[2] < errs[1] < errs[0]
+    assert math.log2(errs[1] / errs[2]) > 1.0
+
+
+def test_oracle_oscillating_lake_mass():
+    """Alg. 3 keeps the mass except for what its dry branch injects (reading A13)."""
+    w = si.c8_oscillating_lake(2, 16)
+    o, d = make_oracle(w)
+    o.set_state(d["h"], d["hu"], d["hv"])
+    m0 = o.info()["mass"] - o.info()["injected_mass"]
+    dt = si.dt_for(w.mesh, w.N, w.g, 0.2, 0.0, 0.2, u_max=0.5)
+    for _ in range(60):
+        assert o.step(dt, 1) == 0
+    i = o.info()
+    assert abs((i["mass"] - i["injected_mass"]) - m0) <= 1e-13 * m0
+    assert i["min_h"] >= 0.0 and i["n_dry"] > 0

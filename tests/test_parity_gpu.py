@@ -257,3 +257,31 @@ def test_set_state_again_reuses_or_rebuilds_layout():
     assert np.array_equal(s.levels(), o.levels())
     assert not np.array_equal(s.levels(), lev1)
     assert_parity(o, s, w.g)
+
+
+def test_parity_couette_annulus():
+    """Couette flow on the annulus (readings A27/A28): curved-boundary walls at r = 2, 4."""
+    w = si.c6_couette(3, 4, 24)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.0, 0.0, 0.2, u_max=0.1)
+    o, s, _ = run_both(w, 100, dt)
+    assert_parity(o, s, w.g)
+
+
+def test_parity_rarefaction_dry_bed():
+    """Rarefaction into a dry bed from the exact state at t = 2 s: PP on, TVB off."""
+    w = si.c7_rarefaction(2, 2)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.0, 0.0, 0.2, u_max=2.0)
+    o, s, _ = run_both(w, 100, dt)
+    assert_parity(o, s, w.g)
+    io, ig = o.info(), s.info()
+    assert io["n_pp"] == ig["n_pp"] > 0 and io["n_dry"] == ig["n_dry"]
+
+
+def test_parity_oscillating_lake():
+    """Oscillating lake: moving wet/dry front, PP + TVB, reflecting walls."""
+    w = si.c8_oscillating_lake(2, 16)
+    dt = si.dt_for(w.mesh, w.N, w.g, 0.2, 0.0, 0.2, u_max=0.5)
+    o, s, _ = run_both(w, 100, dt)
+    assert_parity(o, s, w.g)
+    io, ig = o.info(), s.info()
+    assert io["n_pp"] == ig["n_pp"] > 0 and io["n_dry"] == ig["n_dry"] and io["n_tvb"] == ig["n_tvb"]
