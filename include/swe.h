@@ -101,6 +101,11 @@ typedef struct {
    * level binning still from the binary64 input (bit-exact); parity target 1e-5 against the FP64 oracle
    * (DESIGN.md).  Other values: SWE_ERR_ARG. */
   int32_t precision;
+  /* MRAB inter-level coupling: 0 (default) = reading A17, recursive slowest-first order with coarser
+   * neighbours read mid-step through the AB3 dense output (third order); 1 = Alg. 1's loop nest as
+   * printed (levels descending, substeps inner) with every neighbour at its latest committed
+   * value (SPEC's reading, first order at level interfaces, kept for comparison). */
+  int32_t mrab_coupling;
 } swe_params;
 
 typedef struct {

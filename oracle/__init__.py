@@ -44,7 +44,7 @@ class OrcParams(C.Structure):
     _fields_ = [
         ("h0", C.c_double), ("eps", C.c_double), ("tvb_M", C.c_double), ("tvb_nu", C.c_double),
         ("a_floor", C.c_double), ("eps_u", C.c_double), ("h_char", C.c_double),
-        ("use_pp", C.c_int), ("use_tvb", C.c_int),
+        ("use_pp", C.c_int), ("use_tvb", C.c_int), ("mrab_coupling", C.c_int),
     ]
 
 
@@ -91,7 +91,7 @@ def lib():
         L.orc_refel_get.argtypes = [C.c_int, C.c_char_p, dp]
         L.orc_quad.argtypes = [C.c_int, C.c_int, dp, dp]
         L.orc_set_threads.argtypes = [C.c_int]
-        L.orc_toy_mrab.argtypes = [C.c_int, dp, ip, dp, C.c_double, C.c_int, C.c_int, dp, dp, dp]
+        L.orc_toy_mrab.argtypes = [C.c_int, dp, ip, dp, C.c_double, C.c_int, C.c_int, dp, dp, dp, C.c_int]
         _lib = L
     return _lib
 
@@ -139,7 +139,7 @@ def quad(which: str, q: int):
     return x, w
 
 
-def toy_mrab(A, level, y0, dt, L, nsteps, seed0=None, seed1=None):
+def toy_mrab(A, level, y0, dt, L, nsteps, seed0=None, seed1=None, coupling=0):
     A = _d(A)
     K = A.shape[0]
     lev = np.ascontiguousarray(level, dtype=np.int32)
@@ -152,7 +152,8 @@ def toy_mrab(A, level, y0, dt, L, nsteps, seed0=None, seed1=None):
         s0a, s1a = _d(seed0), _d(seed1)
         s0, s1 = _p(s0a), _p(s1a)
         keep = (s0a, s1a)
-    lib().orc_toy_mrab(K, _p(A), _p(lev, C.c_int), _p(y0), float(dt), int(L), int(nsteps), s0, s1, _p(out))
+    lib().orc_toy_mrab(K, _p(A), _p(lev, C.c_int), _p(y0), float(dt), int(L), int(nsteps), s0, s1, _p(out),
+                       int(coupling))
     del keep
     return out
 
@@ -161,7 +162,7 @@ class Oracle:
     """One oracle solver instance (same calls as the C ABI of the product)."""
 
     def __init__(self, vx, vy, etov, B, N, g, vper=None, h0=1e-6, eps=0.0, tvb_M=0.0, tvb_nu=1.5,
-                 a_floor=0.0, eps_u=0.0, h_char=0.0, use_pp=1, use_tvb=1):
+                 a_floor=0.0, eps_u=0.0, h_char=0.0, use_pp=1, use_tvb=1, mrab_coupling=0):
         L = lib()
         self._vx, self._vy = _d(vx), _d(vy)
         self._etov = np.ascontiguousarray(etov, dtype=np.int32).reshape(-1, 3)
@@ -170,7 +171,7 @@ class Oracle:
         self.Np = (N + 1) * (N + 2) // 2
         self._B = _d(B).reshape(self.K, self.Np)
         self._vper = None if vper is None else np.ascontiguousarray(vper, dtype=np.int32)
-        prm = OrcParams(h0, eps, tvb_M, tvb_nu, a_floor, eps_u, h_char, use_pp, use_tvb)
+        prm = OrcParams(h0, eps, tvb_M, tvb_nu, a_floor, eps_u, h_char, use_pp, use_tvb, mrab_coupling)
         err = C.c_int(0)
         msg = C.create_string_buffer(256)
         self._h = L.orc_create(len(self._vx), _p(self._vx), _p(self._vy), self.K, _p(self._etov, C.c_int),

@@ -74,7 +74,7 @@ void Mrab::init(int K_, int ndof_, int L_, double dt_, const std::vector<int> &l
 void Mrab::state_at(int n, long t, double *out) const {
   int c = level[n];
   const double *q = &Q[(size_t)n * ndof];
-  if (t_e[c] == t) {  // synchronised neighbour: committed value
+  if (coupling == 1 || t_e[c] == t) {  // latest committed (variant) / synchronised neighbour
     for (int i = 0; i < ndof; i++) out[i] = q[i];
     return;
   }
@@ -138,7 +138,12 @@ void Mrab::advance(int l, long t) {
 }
 
 void Mrab::macro_step() {
-  advance(L, tick);
+  if (coupling == 1) {  // Alg. 1 as printed: for l = L..1, for s = 0..Nsteps(l)-1
+    for (int l = L; l >= 1; l--)
+      for (long s = 0; s < (1L << (L - l)); s++) update_level(l, tick + s * (1L << (l - 1)));
+  } else {
+    advance(L, tick);
+  }
   tick += 1L << (L - 1);
 }
 

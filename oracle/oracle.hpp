@@ -76,6 +76,7 @@ int build_mesh(int nverts, const double *vx, const double *vy, int K, const int 
 struct Params {
   double h0 = 1e-6, eps = 0, tvb_M = 0, tvb_nu = 1.5, a_floor = 0, eps_u = 0, h_char = 0;
   int use_pp = 1, use_tvb = 1;
+  int mrab_coupling = 0;  // 0: reading A17 (recursive, dense output); 1: Alg. 1 printed order, latest committed
 };
 
 // ---------------------------------------------------------------- MRAB driver (Alg. 1)
@@ -91,6 +92,10 @@ struct Mrab {
   long tick_s[17] = {0};                      // tick at which level l's current step started
   long t_e[17] = {0};                         // tick of level l's committed state
   long tick = 0;                              // macro-step start, in units of dt
+  // 0: recursive slowest-first order with AB3 dense output (reading A17);
+  // 1: Alg. 1's printed loop nest (levels descending, substeps inner) with every
+  //    neighbour read at its latest committed value (SPEC's reading; first order at level interfaces)
+  int coupling = 0;
   // R(e) at `tick`, may call state_at() for any element
   std::function<void(int e, long tick, double *R)> rhs;
   // hook applied after the AB update of level l (limiters, Alg. 2)

@@ -573,6 +573,7 @@ extern "C" {
 typedef struct {
   double h0, eps, tvb_M, tvb_nu, a_floor, eps_u, h_char;
   int use_pp, use_tvb;
+  int mrab_coupling;
 } orc_params;
 
 typedef struct {
@@ -680,6 +681,7 @@ void *orc_create(int nverts, const double *vx, const double *vy, int K, const in
     s->prm.h_char = p->h_char > 0 ? p->h_char : 10.0 * s->prm.h0;
     s->prm.use_pp = p->use_pp;
     s->prm.use_tvb = p->use_tvb;
+    s->prm.mrab_coupling = p->mrab_coupling;
   } else {
     s->prm.eps = s->prm.h0;
     s->prm.eps_u = 1000.0 * s->prm.h0;
@@ -698,6 +700,7 @@ void *orc_create(int nverts, const double *vx, const double *vy, int K, const in
   s->build_tvb_geometry();
   std::vector<int> lev(K, 1);
   s->mr.init(K, 3 * s->Np, 1, 0.0, lev);
+  s->mr.coupling = s->prm.mrab_coupling;
   return s;
 }
 
@@ -920,8 +923,9 @@ void orc_destroy(void *hnd) { delete (Swe *)hnd; }
 // driver (order pins).  seed0/seed1 (optional): exact R at
 // t0 - 2 dt_l and t0 - dt_l for each element's level (exact AB history).
 int orc_toy_mrab(int K, const double *A, const int *level, const double *y0, double dt, int L, int nsteps,
-                 const double *seed0, const double *seed1, double *yout) {
+                 const double *seed0, const double *seed1, double *yout, int coupling) {
   Mrab mr;
+  mr.coupling = coupling;
   std::vector<int> lev(level, level + K);
   mr.init(K, 1, L, dt, lev);
   for (int e = 0; e < K; e++) mr.Q[e] = y0[e];

@@ -48,7 +48,8 @@ class SweParams(C.Structure):
                 ("use_pp", C.c_int32), ("use_tvb", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", C.c_void_p),
                 ("rank", C.c_int32), ("nranks", C.c_int32), ("owner", C.POINTER(C.c_int32)),
-                ("gid", C.POINTER(C.c_int64)), ("nccl_id", C.c_void_p), ("precision", C.c_int32)]
+                ("gid", C.POINTER(C.c_int64)), ("nccl_id", C.c_void_p), ("precision", C.c_int32),
+                ("mrab_coupling", C.c_int32)]
 
 
 class SweInfo(C.Structure):
@@ -149,6 +150,7 @@ def _params(p: dict | None, device=0, stream=None, alloc=None, part=None) -> Swe
     sp.use_pp = int(p.get("use_pp", 1))
     sp.use_tvb = int(p.get("use_tvb", 1))
     sp.precision = int(p.get("precision", 64))  # 32: FP32 variant
+    sp.mrab_coupling = int(p.get("mrab_coupling", 0))  # 1: Alg. 1 printed order, latest committed (NEXT-4)
     sp.device = int(device)
     sp.stream = stream
     if alloc is not None:

@@ -848,6 +848,12 @@ static int materialize_state(Ctx *c) {
 
 // recursive slowest-first macro step (reading A17):
 // S(l, t) = [(l, t)] + S(l-1, t) + S(l-1, t + 2^(l-2))
+// Alg. 1's loop nest as printed, the mrab_coupling = 1 variant: for l = L..1, substeps inner.
+static void build_schedule_printed(int L, std::vector<std::pair<int, long>> &out) {
+  for (int l = L; l >= 1; l--)
+    for (long s = 0; s < (1L << (L - l)); s++) out.push_back({l, s * (1L << (l - 1))});
+}
+
 static void build_schedule(int l, long t, std::vector<std::pair<int, long>> &out) {
   out.push_back({l, t});
   if (l > 1) {
@@ -905,7 +911,7 @@ static StepParams update_params(Ctx *c, int l, long t) {
   }
   for (int cl = 1; cl <= c->L; cl++) {
     LevelTab &T = p.lev[cl - 1];
-    if (c->t_e[cl] == t) {
+    if (c->prm.mrab_coupling == 1 || c->t_e[cl] == t) {  // latest committed (variant) / synchronised
       T.par = c->par[cl];
       T.dense = 0;
     } else {  // coarser level in the middle of its step
@@ -1070,7 +1076,10 @@ static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
       c->dt = dt;
       c->L = nlevels;
       c->schedule.clear();
-      build_schedule(nlevels, 0, c->schedule);
+      if (c->prm.mrab_coupling == 1)
+        build_schedule_printed(nlevels, c->schedule);
+      else
+        build_schedule(nlevels, 0, c->schedule);
     }
   } else {
     for (Ctx *c : G)
@@ -1214,6 +1223,10 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
     swe_destroy(h);
     return rc;
   };
+  if (c->prm.mrab_coupling != 0 && c->prm.mrab_coupling != 1) {
+    c->err = "mrab_coupling must be 0 or 1";
+    return fail(SWE_ERR_ARG);
+  }
   if (c->prm.precision != 0 && c->prm.precision != 32 && c->prm.precision != 64) {
     c->err = "precision must be 32 or 64";
     return fail(SWE_ERR_ARG);

@@ -16,7 +16,7 @@ from tests.common import make_oracle
 GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "limiter_examples.json")))
 
 
-def _toy_errors(A, level, L, T, dts, seeded):
+def _toy_errors(A, level, L, T, dts, seeded, coupling=0):
     K = A.shape[0]
     y0 = np.linspace(1.0, 0.5, K)
     errs = []
@@ -28,7 +28,7 @@ def _toy_errors(A, level, L, T, dts, seeded):
             h = dt * 2.0 ** (lev - 1)
             s0 = np.array([(A @ expm(-2 * h[e] * A) @ y0)[e] for e in range(K)])
             s1 = np.array([(A @ expm(-1 * h[e] * A) @ y0)[e] for e in range(K)])
-        y = oracle.toy_mrab(A, level, y0, dt, L, nsteps, s0, s1)
+        y = oracle.toy_mrab(A, level, y0, dt, L, nsteps, s0, s1, coupling=coupling)
         errs.append(np.abs(y - expm(T * A) @ y0).max())
     return np.array(errs)
 
@@ -51,6 +51,24 @@ def test_mrab_three_level_order():
     assert np.all(np.abs(np.log2(e[:-1] / e[1:]) - 3.0) < 0.15)
     e = _toy_errors(A, level, 3, 2.0, dts, seeded=False)
     assert np.all(np.log2(e[:-1] / e[1:]) > 1.85)
+
+
+def test_mrab_printed_order_latest_committed_is_first_order():
+    """The variant (SPEC's reading of Alg. 1): the printed loop nest (levels
+    descending, substeps inner) with every neighbour at its latest committed value.
+    Coupled levels see each other up to one coarse step out of sync, so the scheme is first order
+    (SPEC S:419 reports 0.99), while uncoupled levels keep AB3's third order."""
+    A = np.array([[-1.0, 0.5, 0.0], [0.3, -0.8, 0.4], [0.0, 0.6, -0.5]])
+    dts = [0.02, 0.01, 0.005]
+    e = _toy_errors(A, [1, 2, 3], 3, 2.0, dts, seeded=True, coupling=1)
+    assert np.all(np.abs(np.log2(e[:-1] / e[1:]) - 1.0) < 0.1)
+    Ad = np.diag([-1.0, -0.8, -0.5])  # no coupling: each level is plain AB3
+    e = _toy_errors(Ad, [1, 2, 3], 3, 2.0, dts, seeded=True, coupling=1)
+    assert np.all(np.abs(np.log2(e[:-1] / e[1:]) - 3.0) < 0.15)
+    # one level: identical to the default schedule
+    y1 = oracle.toy_mrab(A, [1, 1, 1], [1.0, 2.0, 0.5], 0.01, 1, 40, coupling=1)
+    y0 = oracle.toy_mrab(A, [1, 1, 1], [1.0, 2.0, 0.5], 0.01, 1, 40, coupling=0)
+    assert np.array_equal(y1, y0)
 
 
 def test_single_level_is_textbook_ab3():

@@ -285,3 +285,15 @@ def test_parity_oscillating_lake():
     assert_parity(o, s, w.g)
     io, ig = o.info(), s.info()
     assert io["n_pp"] == ig["n_pp"] > 0 and io["n_dry"] == ig["n_dry"] and io["n_tvb"] == ig["n_tvb"]
+
+
+def test_parity_mrab_printed_order_variant():
+    """mrab_coupling = 1: Alg. 1's printed loop order with latest committed
+    neighbours, on the C4 wet/dry MRAB case; it differs from the default coupling."""
+    w = si.c4_dambreak(N=3, base=5)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    o, s, _ = run_both(w, 8, dt, nlevels=3, mrab_coupling=1)
+    assert np.array_equal(o.levels(), s.levels())
+    assert_parity(o, s, w.g)
+    _, s0, _ = run_both(w, 8, dt, nlevels=3)
+    assert max(parity_rel(s.get_state(), s0.get_state(), w.g)) > 1e-10  # far above the 1e-12 parity level
