@@ -149,6 +149,13 @@ int swe_step(swe_ctx *ctx, double dt, int nlevels);
 /* Copy the current state to the host, caller order, [nelems*Np] each. */
 int swe_get_state(swe_ctx *ctx, double *h, double *hu, double *hv);
 
+/* Level regrouping ("elements can be regrouped after every few time steps"):
+ * the current state becomes the state of a fresh swe_set_state -- levels re-binned at the next
+ * swe_step (which may use a new dt and nlevels), Alg. 2 line 1 applied to it, AB ramp and counters
+ * restarted -- while swe_info.t continues.  Single-rank contexts (nranks <= 1) only: SWE_ERR_ARG
+ * otherwise; SWE_ERR_STATE before swe_set_state. */
+int swe_regroup(swe_ctx *ctx);
+
 void swe_destroy(swe_ctx *ctx); /* NULL-safe; frees all device memory */
 
 /* ------------------------------------------------------------ multi-rank */

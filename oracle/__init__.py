@@ -91,6 +91,7 @@ def lib():
         L.orc_refel_get.argtypes = [C.c_int, C.c_char_p, dp]
         L.orc_quad.argtypes = [C.c_int, C.c_int, dp, dp]
         L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_regroup.argtypes = [C.c_void_p]
         L.orc_toy_mrab.argtypes = [C.c_int, dp, ip, dp, C.c_double, C.c_int, C.c_int, dp, dp, dp, C.c_int]
         _lib = L
     return _lib
@@ -196,6 +197,12 @@ class Oracle:
 
     def step(self, dt, nlevels=1):
         return lib().orc_step(self._h, float(dt), int(nlevels))
+
+    def regroup(self):
+        """Re-bin the levels from the current state at the next step; time continues."""
+        rc = lib().orc_regroup(self._h)
+        if rc != 0:
+            raise RuntimeError(f"orc_regroup failed ({rc})")
 
     def get_state(self):
         h, hu, hv = (np.zeros((self.K, self.Np)) for _ in range(3))

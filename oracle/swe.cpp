@@ -41,6 +41,7 @@ struct Swe {
   Mrab mr;                  // holds the state in mr.Q, element-major [e][field][node]
   bool have_state = false, scheduled = false;
   double sched_dt = 0;
+  double t_base = 0;  // simulated time carried across swe_regroup (P:149 regrouping)
   int sched_L = 0;
   std::vector<int> dry;
   std::vector<TvbEdge> tvb;  // K*3
@@ -723,6 +724,7 @@ int orc_set_state(void *hnd, const double *h, const double *hu, const double *hv
   s->injected = 0;
   s->have_state = true;
   s->scheduled = false;
+  s->t_base = 0;
   // Alg. 2 line 1: Q^0 = Lambda Pi M Pi (Pi_H Q^0) on every element
   std::vector<int> all(K);
   for (int e = 0; e < K; e++) all[e] = e;
@@ -754,6 +756,23 @@ int orc_step(void *hnd, double dt, int nlevels) {
   s->mr.macro_step();
   for (double v : s->mr.Q)
     if (!std::isfinite(v)) return -6;
+  return 0;
+}
+
+// Level regrouping ("elements can be regrouped after every few time steps"; SURVEY
+// NEXT-4): the current state becomes the state of a fresh swe_set_state -- levels re-binned at
+// the next step from it, Alg. 2 line 1 applied to it, AB ramp and counters restarted -- while the
+// simulated time continues.
+int orc_get_state(void *hnd, double *h, double *hu, double *hv);
+int orc_regroup(void *hnd) {
+  Swe *s = (Swe *)hnd;
+  if (!s->have_state) return -4;
+  const double t = s->t_base + (s->scheduled ? s->sched_dt * (double)s->mr.tick : 0.0);
+  const size_t KNp = (size_t)s->K * s->Np;
+  std::vector<double> h(KNp), hu(KNp), hv(KNp);
+  orc_get_state(hnd, h.data(), hu.data(), hv.data());
+  orc_set_state(hnd, h.data(), hu.data(), hv.data());
+  s->t_base = t;
   return 0;
 }
 
@@ -873,7 +892,7 @@ int orc_get_info(void *hnd, orc_info *info) {
   info->K = s->K;
   info->Np = s->Np;
   info->nlevels = s->scheduled ? s->sched_L : 0;
-  info->t = s->scheduled ? s->sched_dt * (double)s->mr.tick : 0.0;
+  info->t = s->t_base + (s->scheduled ? s->sched_dt * (double)s->mr.tick : 0.0);
   double mass = 0, minh = std::numeric_limits<double>::infinity();
   for (int e = 0; e < s->K; e++) {
     const double *q = &s->mr.Q[(size_t)e * 3 * s->Np];

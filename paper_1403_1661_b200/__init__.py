@@ -20,7 +20,8 @@ SWE_ERRORS = {0: "SWE_OK", -1: "SWE_ERR_ARG", -2: "SWE_ERR_MESH", -3: "SWE_ERR_O
               -5: "SWE_ERR_SCHEDULE", -6: "SWE_ERR_NONFINITE", -7: "SWE_ERR_CUDA", -8: "SWE_ERR_NCCL",
               -9: "SWE_ERR_NOMEM"}
 
-EXPORTED = ["swe_nodes", "swe_create", "swe_set_state", "swe_step", "swe_get_state", "swe_destroy", "swe_get_levels",
+EXPORTED = ["swe_nodes", "swe_create", "swe_set_state", "swe_step", "swe_get_state", "swe_regroup", "swe_destroy",
+            "swe_get_levels",
             "swe_get_connectivity", "swe_get_info", "swe_last_error", "swe_profile", "swe_profile_read",
             "swe_nccl_unique_id", "swe_link_group", "swe_step_group",
             "swe_host_refel", "swe_host_connectivity", "swe_host_hk", "swe_host_levels", "swe_host_tvb_geometry",
@@ -80,6 +81,7 @@ def lib():
         L.swe_create.argtypes = [C.POINTER(SweMesh), dp, C.c_int, C.c_double, C.POINTER(SweParams), C.POINTER(vp)]
         L.swe_set_state.argtypes = [vp, dp, dp, dp]
         L.swe_step.argtypes = [vp, C.c_double, C.c_int]
+        L.swe_regroup.argtypes = [vp]
         L.swe_get_state.argtypes = [vp, dp, dp, dp]
         L.swe_destroy.argtypes = [vp]
         L.swe_destroy.restype = None
@@ -316,6 +318,10 @@ class Solver:
         h, hu, hv = out
         _check(lib().swe_get_state(self._h, _p(h), _p(hu), _p(hv)), self._h)
         return h, hu, hv
+
+    def regroup(self):
+        """Re-bin the levels from the current state at the next step; time continues."""
+        _check(lib().swe_regroup(self._h), self._h)
 
     def get_state_into(self, h, hu, hv):
         """Write into caller-provided (e.g. pinned) contiguous float64 buffers of K*Np elements."""

@@ -225,6 +225,7 @@ struct Ctx {
   bool have_state = false, materialized = false, scheduled = false;
   bool layout_valid = false;  // internal order + static tables match c->level / c->L
   double dt = 0.0;
+  double t_base = 0.0;  // simulated time carried across swe_regroup
   int L = 1;
   std::vector<int32_t> level;  // given-mesh order
   std::vector<int32_t> order;  // internal k -> given-mesh e (owned first, then ghosts)
@@ -1331,6 +1332,7 @@ int swe_set_state(swe_ctx *h, const double *hh, const double *hu, const double *
   c->scheduled = false;
   c->n_updates = 0;
   c->tick = 0;
+  c->t_base = 0.0;
   return SWE_OK;
 }
 
@@ -1368,6 +1370,38 @@ int swe_step_group(swe_ctx **ctxs, int n, double dt, int nlevels) {
   }
   std::vector<Ctx *> G = c0->group;
   return group_step(G, dt, nlevels);
+}
+
+int swe_regroup(swe_ctx *h) {
+  if (!h) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  if (!c->have_state) return SWE_ERR_STATE;
+  if (c->nranks > 1) {
+    c->err = "swe_regroup: single-rank contexts only";
+    return SWE_ERR_ARG;
+  }
+  if (!c->materialized) return SWE_OK;  // nothing stepped since swe_set_state: the staged state stands
+  // current state -> staging (caller order), then the swe_set_state path from there
+  const size_t KNp = (size_t)c->Kin * c->Np;
+  GatherParams g = gather_params(c, c->dStage, c->dStage + KNp, c->dStage + 2 * KNp);
+  if (c->f32)
+    k_gather_state<float><<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
+  else
+    k_gather_state<double><<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
+  CK(cudaGetLastError());
+  const double t = c->t_base + (c->scheduled ? c->dt * (double)c->tick : 0.0);
+  double e2 = c->prm.eps_u * c->prm.eps_u, e4 = e2 * e2;
+  k_speeds<<<(c->Kin + 127) / 128, 128, 0, c->stream>>>(c->Kin, c->Np, c->g, e4, c->prm.a_floor, c->dStage,
+                                                         c->dStage + KNp, c->dStage + 2 * KNp, c->dAe);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
+  CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream));
+  c->materialized = false;
+  c->scheduled = false;
+  c->n_updates = 0;
+  c->tick = 0;
+  c->t_base = t;
+  return SWE_OK;
 }
 
 int swe_get_state(swe_ctx *h, double *hh, double *hu, double *hv) {
@@ -1459,7 +1493,7 @@ int swe_get_info(swe_ctx *h, swe_info *info) {
   info->N = c->N;
   info->nflipped = c->mesh.nflipped;
   info->nlevels = c->scheduled ? c->L : 0;
-  info->t = c->scheduled ? c->dt * (double)c->tick : 0.0;
+  info->t = c->t_base + (c->scheduled ? c->dt * (double)c->tick : 0.0);
   info->n_updates = c->n_updates;
   if (c->scheduled)
     for (int l = 1; l <= c->L; l++) info->level_count[l - 1] = c->off[l] - c->off[l - 1];

@@ -205,3 +205,26 @@ def test_thacker_mass_positivity_accuracy():
     he, _, _ = ex(d["x"], d["y"], nsteps * dt)
     assert np.abs(h - he).max() < 0.05 * he.max()
     assert np.abs(o.get_state()[0][:, 0] * 0 + GOLDEN["thacker_h_origin"]["h"] - ex(0.0, 0.0, 0.0)[0]).max() < 1e-12
+
+
+def test_oracle_regroup_is_set_state_of_the_current_state():
+    """Level regrouping: identical to swe_set_state of the current state, except that the
+    simulated time continues."""
+    w = si.c4_dambreak(N=2, base=10)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    a, d = make_oracle(w)
+    b, _ = make_oracle(w)
+    for o in (a, b):
+        o.set_state(d["h"], d["hu"], d["hv"])
+        for _ in range(3):
+            assert o.step(dt, 3) == 0
+    t1 = a.info()["t"]
+    a.regroup()
+    b.set_state(*b.get_state())
+    for o in (a, b):
+        for _ in range(2):
+            assert o.step(0.5 * dt, 2) == 0
+    for x, y in zip(a.get_state(), b.get_state()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a.levels(), b.levels())
+    assert abs(a.info()["t"] - (t1 + b.info()["t"])) < 1e-12 * t1

@@ -297,3 +297,19 @@ def test_parity_mrab_printed_order_variant():
     assert_parity(o, s, w.g)
     _, s0, _ = run_both(w, 8, dt, nlevels=3)
     assert max(parity_rel(s.get_state(), s0.get_state(), w.g)) > 1e-10  # far above the 1e-12 parity level
+
+
+def test_parity_regroup():
+    """swe_regroup (NEXT-4): re-binned levels, restarted ramp, continued time; against the
+    oracle's regroup, with a new (dt, nlevels) after the regroup."""
+    w = si.c4_dambreak(N=3, base=5)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    o, s, d = run_both(w, 4, dt, nlevels=3)
+    o.regroup()
+    s.regroup()
+    for _ in range(4):
+        assert o.step(0.5 * dt, 2) == 0
+        s.step(0.5 * dt, 2)
+    assert np.array_equal(o.levels(), s.levels())
+    assert_parity(o, s, w.g)
+    assert abs(o.info()["t"] - s.info()["t"]) <= 1e-12 * o.info()["t"]
