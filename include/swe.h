@@ -63,6 +63,10 @@ typedef struct {
   int32_t nelems;
   const int32_t *etov;        /* [nelems*3], 0-based vertex indices */
   const int32_t *vperiodic;   /* [nverts] or NULL */
+  /* Boundary tags [nverts] or NULL (reading A7'): an unmatched face whose two vertices are both
+   * tagged 1 is a transmissive outflow boundary (ghost state = interior trace, TVB ghost mean =
+   * own mean); every other unmatched face is a reflective wall. */
+  const int8_t *vbc;
 } swe_mesh;
 
 /* Parameters; a zero-initialised struct (or NULL) selects the defaults. */

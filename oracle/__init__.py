@@ -92,6 +92,7 @@ def lib():
         L.orc_quad.argtypes = [C.c_int, C.c_int, dp, dp]
         L.orc_set_threads.argtypes = [C.c_int]
         L.orc_regroup.argtypes = [C.c_void_p]
+        L.orc_set_boundary.argtypes = [C.c_void_p, C.c_void_p]
         L.orc_toy_mrab.argtypes = [C.c_int, dp, ip, dp, C.c_double, C.c_int, C.c_int, dp, dp, dp, C.c_int]
         _lib = L
     return _lib
@@ -163,7 +164,7 @@ class Oracle:
     """One oracle solver instance (same calls as the C ABI of the product)."""
 
     def __init__(self, vx, vy, etov, B, N, g, vper=None, h0=1e-6, eps=0.0, tvb_M=0.0, tvb_nu=1.5,
-                 a_floor=0.0, eps_u=0.0, h_char=0.0, use_pp=1, use_tvb=1, mrab_coupling=0):
+                 a_floor=0.0, eps_u=0.0, h_char=0.0, use_pp=1, use_tvb=1, mrab_coupling=0, vbc=None):
         L = lib()
         self._vx, self._vy = _d(vx), _d(vy)
         self._etov = np.ascontiguousarray(etov, dtype=np.int32).reshape(-1, 3)
@@ -180,6 +181,9 @@ class Oracle:
                                C.byref(prm), C.byref(err), msg, 256)
         if not self._h:
             raise ValueError(f"orc_create failed ({err.value}): {msg.value.decode()}")
+        if vbc is not None:  # vertex boundary tags: 1 = transmissive outflow (reading A7')
+            self._vbc = np.ascontiguousarray(vbc, dtype=np.int8)
+            L.orc_set_boundary(self._h, self._vbc.ctypes.data_as(C.c_void_p))
 
     def __del__(self):
         if getattr(self, "_h", None):

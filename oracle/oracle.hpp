@@ -67,6 +67,7 @@ struct Mesh {
   std::vector<int> EToE, EToF;    // K*3, boundary: self reference
   std::vector<double> J, rx, ry, sx, sy, area, Hk;
   std::vector<double> nx, ny, sJ;  // K*3, face f = v_f -> v_{f+1}
+  std::vector<signed char> bc;     // K*3, boundary faces: 0 reflective wall, 1 transmissive outflow (A7')
 };
 // returns 0, or -2 (mesh error) with msg filled
 int build_mesh(int nverts, const double *vx, const double *vy, int K, const int *etov,

@@ -172,10 +172,12 @@ void Swe::rhs(int e, const std::function<void(int, double *)> &nbr, const double
   double qn[3 * NPMAX];
   for (int f = 0; f < 3; f++) {
     int n = mesh.EToE[3 * (size_t)e + f], nf = mesh.EToF[3 * (size_t)e + f];
-    bool wall = (n == e && nf == f);
+    bool bnd = (n == e && nf == f);
+    bool outflow = bnd && !mesh.bc.empty() && mesh.bc[3 * (size_t)e + f] == 1;
+    bool wall = bnd && !outflow;
     double nx = mesh.nx[3 * (size_t)e + f], ny = mesh.ny[3 * (size_t)e + f];
     double scale = mesh.sJ[3 * (size_t)e + f] / J;
-    if (!wall) nbr(n, qn);
+    if (!bnd) nbr(n, qn);
     const double *bn = &B[(size_t)n * Np];
     for (int j = 0; j < Ng; j++) {
       int gm = f * Ng + j;
@@ -187,6 +189,11 @@ void Swe::rhs(int e, const std::function<void(int, double *)> &nbr, const double
         bp = bm;
         hup = hum - 2.0 * mn * nx;
         hvp = hvm - 2.0 * mn * ny;
+      } else if (outflow) {  // transmissive ghost (A7'): the interior trace itself
+        hp = hm;
+        bp = bm;
+        hup = hum;
+        hvp = hvm;
       } else {  // neighbour's Gauss points run in the opposite direction
         int gpn = nf * Ng + (Ng - 1 - j);
         double a[4] = {0, 0, 0, 0};
@@ -481,7 +488,9 @@ void Swe::tvb_apply(const std::vector<int> &E) {
       for (int p = 0; p < 2; p++) {
         int f = slots[p];
         int n = mesh.EToE[3 * (size_t)e + f], nf = mesh.EToF[3 * (size_t)e + f];
-        if (n == e && nf == f) {  // wall ghost mean
+        if (n == e && nf == f && !mesh.bc.empty() && mesh.bc[3 * (size_t)e + f] == 1) {  // outflow ghost mean
+          for (int k = 0; k < 3; k++) nm[p][k] = qb[k];
+        } else if (n == e && nf == f) {  // wall ghost mean
           double nx = mesh.nx[3 * (size_t)e + f], ny = mesh.ny[3 * (size_t)e + f];
           double mn = qb[1] * nx + qb[2] * ny;
           nm[p][0] = qb[0];
@@ -763,6 +772,23 @@ int orc_step(void *hnd, double dt, int nlevels) {
 // NEXT-4): the current state becomes the state of a fresh swe_set_state -- levels re-binned at
 // the next step from it, Alg. 2 line 1 applied to it, AB ramp and counters restarted -- while the
 // simulated time continues.
+// Boundary tags (reading A7'): an unmatched face whose two vertices are both tagged 1 is a
+// transmissive outflow boundary (ghost state = interior trace); every other unmatched face stays a
+// reflective wall.  vbc = NULL: all walls.
+int orc_set_boundary(void *hnd, const signed char *vbc) {
+  Swe *s = (Swe *)hnd;
+  s->mesh.bc.assign((size_t)3 * s->K, 0);
+  if (!vbc) return 0;
+  for (int e = 0; e < s->K; e++)
+    for (int f = 0; f < 3; f++) {
+      const size_t i = 3 * (size_t)e + f;
+      if (s->mesh.EToE[i] != e || s->mesh.EToF[i] != f) continue;
+      const int a = s->mesh.EToV[3 * (size_t)e + f], b = s->mesh.EToV[3 * (size_t)e + (f + 1) % 3];
+      s->mesh.bc[i] = (vbc[a] == 1 && vbc[b] == 1) ? 1 : 0;
+    }
+  return 0;
+}
+
 int orc_get_state(void *hnd, double *h, double *hu, double *hv);
 int orc_regroup(void *hnd) {
   Swe *s = (Swe *)hnd;

@@ -36,7 +36,8 @@ class SweError(RuntimeError):
 
 class SweMesh(C.Structure):
     _fields_ = [("nverts", C.c_int32), ("vx", C.POINTER(C.c_double)), ("vy", C.POINTER(C.c_double)),
-                ("nelems", C.c_int32), ("etov", C.POINTER(C.c_int32)), ("vperiodic", C.POINTER(C.c_int32))]
+                ("nelems", C.c_int32), ("etov", C.POINTER(C.c_int32)), ("vperiodic", C.POINTER(C.c_int32)),
+                ("vbc", C.POINTER(C.c_int8))]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -121,13 +122,15 @@ def _p(a, t=C.c_double):
 class _MeshArgs:
     """Keeps the numpy buffers of a swe_mesh alive."""
 
-    def __init__(self, vx, vy, etov, vper=None):
+    def __init__(self, vx, vy, etov, vper=None, vbc=None):
         self.vx, self.vy = _d(vx), _d(vy)
         self.etov = np.ascontiguousarray(etov, dtype=np.int32).reshape(-1, 3)
         self.vper = None if vper is None else np.ascontiguousarray(vper, dtype=np.int32)
+        self.vbc = None if vbc is None else np.ascontiguousarray(vbc, dtype=np.int8)
         self.K = self.etov.shape[0]
         self.s = SweMesh(len(self.vx), _p(self.vx), _p(self.vy), self.K, _p(self.etov, C.c_int32),
-                         _p(self.vper, C.c_int32) if self.vper is not None else C.POINTER(C.c_int32)())
+                         _p(self.vper, C.c_int32) if self.vper is not None else C.POINTER(C.c_int32)(),
+                         _p(self.vbc, C.c_int8) if self.vbc is not None else C.POINTER(C.c_int8)())
 
 
 def _check(rc, ctx=None):
@@ -262,10 +265,10 @@ class _TorchAllocator:
 class Solver:
     """One solver context (swe_create ... swe_destroy)."""
 
-    def __init__(self, vx, vy, etov, B, N, g, vper=None, params: dict | None = None, device: int = 0,
+    def __init__(self, vx, vy, etov, B, N, g, vper=None, params: dict | None = None, device: int = 0, vbc=None,
                  use_torch: bool = True, rank: int = 0, nranks: int = 1, owner=None, gid=None, nccl_id=None):
         L = lib()
-        self._mesh = _MeshArgs(vx, vy, etov, vper)
+        self._mesh = _MeshArgs(vx, vy, etov, vper, vbc)
         self.K = self._mesh.K
         self.N = N
         self.Np = (N + 1) * (N + 2) // 2

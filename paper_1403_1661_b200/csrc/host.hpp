@@ -45,7 +45,10 @@ struct HostMesh {
   std::vector<int32_t> etoe;   // K*3
   std::vector<int8_t> etof;    // K*3
   std::vector<double> hk;      // incircle diameter
+  std::vector<int8_t> bc;      // K*3: boundary faces 0 reflective wall, 1 transmissive outflow (A7')
 };
+// Outflow tags from vertex tags (swe_mesh.vbc, NULL = all walls).
+void apply_boundary_tags(HostMesh &m, const int8_t *vbc);
 // returns 0 or SWE_ERR_MESH (-2)
 int build_mesh(int nverts, const double *vx, const double *vy, int K, const int32_t *etov,
                const int32_t *vper, HostMesh &m, std::string *err);

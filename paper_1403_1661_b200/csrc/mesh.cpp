@@ -335,4 +335,16 @@ void build_halo_plan(const HostMesh &m, const int64_t *gid, const int32_t *owner
   std::sort(plan.ghosts.begin(), plan.ghosts.end(), by_gid);
 }
 
+void apply_boundary_tags(HostMesh &m, const int8_t *vbc) {
+  m.bc.assign((size_t)3 * m.K, 0);
+  if (!vbc) return;
+  for (int e = 0; e < m.K; e++)
+    for (int f = 0; f < 3; f++) {
+      const size_t i = (size_t)3 * e + f;
+      if (m.etoe[i] != e || m.etof[i] != f) continue;  // interior face
+      const int a = m.etov[(size_t)3 * e + f], b = m.etov[(size_t)3 * e + (f + 1) % 3];
+      m.bc[i] = (vbc[a] == 1 && vbc[b] == 1) ? 1 : 0;
+    }
+}
+
 }  // namespace swe

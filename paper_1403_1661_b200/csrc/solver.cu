@@ -773,7 +773,10 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
           c->err = "owned element with a neighbour outside the local set";
           return SWE_ERR_MESH;
         }
-        E2E[(size_t)f * K + k] = (inv[n] << 2) | nf;
+        // boundary faces are self references (n == e, nf == f); a transmissive outflow face (A7')
+        // carries neighbour face code 3 instead
+        const bool outflow = n == e && nf == f && c->mesh.bc[(size_t)3 * e + f] == 1;
+        E2E[(size_t)f * K + k] = (inv[n] << 2) | (outflow ? 3 : nf);
       } else {
         E2E[(size_t)f * K + k] = (k << 2) | f;  // ghosts are never launched
       }
@@ -1237,6 +1240,7 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   if (c->rank < 0 || c->rank >= c->nranks) return fail(SWE_ERR_ARG);
   int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, c->mesh, &c->err);
   if (rc) return fail(rc);
+  apply_boundary_tags(c->mesh, mesh->vbc);
   if (!build_refops(N, c->ops, &c->err)) return fail(SWE_ERR_ORDER);
   for (int f = 0; f < 3; f++)
     for (int k = 0; k < c->ops.Nfp; k++)

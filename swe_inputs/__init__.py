@@ -57,6 +57,7 @@ class Mesh:
     etov: np.ndarray            # (K, 3) int32
     vper: np.ndarray | None = None   # canonical vertex ids for periodic face matching
     gen: np.ndarray | None = None    # NVB generation per element (graded meshes)
+    vbc: np.ndarray | None = None    # vertex boundary tags: 1 = transmissive outflow (reading A7')
 
     @property
     def K(self) -> int:
@@ -119,7 +120,7 @@ def shuffle(mesh: Mesh, seed: int = SEED, rotate: bool = True, flip_fraction: fl
         flip = rng.random(mesh.K) < flip_fraction
         etov[flip] = etov[flip][:, [0, 2, 1]]
     gen = None if mesh.gen is None else mesh.gen[perm]
-    return Mesh(mesh.vx, mesh.vy, np.ascontiguousarray(etov, dtype=np.int32), mesh.vper, gen)
+    return Mesh(mesh.vx, mesh.vy, np.ascontiguousarray(etov, dtype=np.int32), mesh.vper, gen, mesh.vbc)
 
 
 # ------------------------------------------------------------------ workloads
@@ -320,6 +321,24 @@ def c7_rarefaction(N: int = 2, n: int = 1, t0: float = 2.0, shuffle_seed: int | 
     prm = dict(h0=1e-6, use_pp=1, use_tvb=0)
     w = Workload(f"Rarefaction-n{n}", m, N, 1.0, lambda x, y: np.zeros_like(x), lambda x, y: ex(x, y, t0), prm,
                  1, 0.2, 0, ex)
+    w.t0 = t0
+    return w
+
+
+def c7_rarefaction_outflow(N: int = 2, n: int = 2, outflow: bool = True, t0: float = 2.0,
+                           shuffle_seed: int | None = SEED) -> Workload:
+    """The rarefaction on the short box [0, 30] x [0, 8] whose right side x = 30 is a
+    transmissive outflow boundary (reading A7'; outflow=False: a wall): the dry front leaves the
+    domain at t = 5 s and the fan keeps matching the exact solution.  2 x (6 n) x (2 n) triangles."""
+    m = structured(6 * n, 2 * n, 0.0, 30.0, 0.0, 8.0)
+    if outflow:
+        m.vbc = (np.abs(m.vx - 30.0) < 1e-12).astype(np.int8)
+    if shuffle_seed is not None:
+        m = shuffle(m, shuffle_seed)
+    ex = rarefaction_exact()
+    prm = dict(h0=1e-6, use_pp=1, use_tvb=0)
+    w = Workload(f"RarefactionOut-n{n}-{'out' if outflow else 'wall'}", m, N, 1.0, lambda x, y: np.zeros_like(x),
+                 lambda x, y: ex(x, y, t0), prm, 1, 0.2, 0, ex)
     w.t0 = t0
     return w
 

@@ -21,7 +21,7 @@ def make_oracle(w: si.Workload, **over):
     x, y = probe.nodes()
     del probe
     B, h, hu, hv = w.fields(x, y)
-    o = oracle.Oracle(m.vx, m.vy, m.etov, B, w.N, w.g, vper=m.vper, **prm)
+    o = oracle.Oracle(m.vx, m.vy, m.etov, B, w.N, w.g, vper=m.vper, vbc=m.vbc, **prm)
     return o, dict(x=x, y=y, B=B, h=h, hu=hu, hv=hv)
 
 

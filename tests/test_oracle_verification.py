@@ -155,3 +155,20 @@ def test_oracle_oscillating_lake_mass():
     i = o.info()
     assert abs((i["mass"] - i["injected_mass"]) - m0) <= 1e-13 * m0
     assert i["min_h"] >= 0.0 and i["n_dry"] > 0
+
+
+# ------------------------------------------------------------------ transmissive outflow boundary
+def test_oracle_outflow_boundary_lets_the_rarefaction_leave():
+    """Reading A7' (the transmissive half of NEXT-3): on the short box [0,30] x [0,8] the fan
+    crosses x = 30 at t = 5 s.  With the outflow boundary the solution next to it keeps converging
+    to the exact one; a reflective wall there sends a reflected wave back and does not converge."""
+    def err(outflow, n, T=8.0):
+        w = si.c7_rarefaction_outflow(2, n, outflow)
+        o, _ = _run(w, T, t0=2.0, u_max=2.0)
+        assert o.get_state()[0].min() >= 0.0
+        return _l2(o, w, T, region=lambda x, y: (x > 20.0) & (x < 30.0))
+
+    out2, out4 = err(True, 2), err(True, 4)
+    wall4 = err(False, 4)
+    assert math.log2(out2 / out4) > 1.5
+    assert out4 < 0.1 * wall4

@@ -29,7 +29,7 @@ def make_pair(w, **over):
     prm = dict(w.params)
     prm.update(over)
     m = w.mesh
-    s = P.Solver(m.vx, m.vy, m.etov, d["B"], w.N, w.g, vper=m.vper, params=prm)
+    s = P.Solver(m.vx, m.vy, m.etov, d["B"], w.N, w.g, vper=m.vper, params=prm, vbc=m.vbc)
     return o, s, d
 
 
@@ -313,3 +313,13 @@ def test_parity_regroup():
     assert np.array_equal(o.levels(), s.levels())
     assert_parity(o, s, w.g)
     assert abs(o.info()["t"] - s.info()["t"]) <= 1e-12 * o.info()["t"]
+
+
+def test_parity_outflow_boundary():
+    """Transmissive outflow boundary (reading A7'): the rarefaction started at t = 4.8 s crosses
+    x = 30 within the run; PP on."""
+    w = si.c7_rarefaction_outflow(2, 4, True, t0=4.8)
+    assert w.mesh.vbc is not None and w.mesh.vbc.sum() > 0
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.0, 0.0, 0.2, u_max=2.0)
+    o, s, _ = run_both(w, 150, dt)
+    assert_parity(o, s, w.g)
