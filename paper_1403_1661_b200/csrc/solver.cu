@@ -237,9 +237,21 @@ struct Ctx {
   long n_updates = 0;
   std::vector<std::pair<int, long>> schedule;  // (level, tick offset) of one macro step
   StepParams cur;  // parameters of the update in flight
+  // CUDA graphs of whole macro steps (single rank): the launch sequence repeats with period 6 after the
+  // AB ramp (ring slot mod 3, Q parity mod 2), so each distinct parameter sequence is captured once
+  struct StepGraph {
+    std::vector<StepParams> seq;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<StepGraph> graphs;
+  bool use_graphs = true;
+  cudaStream_t gstream = nullptr;          // private non-blocking stream: graphs are captured and replayed here
+  cudaEvent_t gev0 = nullptr, gev1 = nullptr;  // order gstream after / before the caller's stream
   // profiling
   bool prof = false;
-  std::vector<cudaEvent_t> ev;
+  std::vector<cudaEvent_t> ev;      // (start, stop) pairs recorded this macro step
+  std::vector<cudaEvent_t> evpool;  // created once, reused
+  size_t evnext = 0;
   double prof_ms[2] = {0, 0}, prof_bytes[2] = {0, 0};
   long prof_launch[2] = {0, 0};
   bool alloc_ok = true;
@@ -711,12 +723,14 @@ static void order_subset(const HostMesh &m, const std::vector<int32_t> &levels, 
 // scatter the staged unlimited state, reset the MRAB schedule.  The initial
 // limiting (Alg. 2 line 1) is applied by init_limit_* (group-aware).
 static int materialize_state(Ctx *c);
+static void clear_graphs(Ctx *c);
 static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   const int K = c->K;
   // The layout (internal order, connectivity, geometry, exchange tables) depends only on the
   // levels: a new state that bins to the resident levels reuses it and only scatters the state.
   if (c->layout_valid && c->L == L && c->level == levels) return materialize_state(c);
   c->layout_valid = false;
+  clear_graphs(c);
   c->level = levels;
   c->L = L;
   std::vector<int32_t> owned_sorted, ghosts_sorted;
@@ -944,9 +958,13 @@ static void launch_timed(Ctx *c, int which, const StepParams &p) {
   const int nel = p.k1 - p.k0;
   if (nel <= 0) return;
   if (c->prof) {
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    while (c->evpool.size() < c->evnext + 2) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->evpool.push_back(e);
+    }
+    cudaEvent_t e0 = c->evpool[c->evnext], e1 = c->evpool[c->evnext + 1];
+    c->evnext += 2;
     cudaEventRecord(e0, c->stream);
     launch(which, false, c->N, p, c->stream, c->f32);
     cudaEventRecord(e1, c->stream);
@@ -967,8 +985,127 @@ static void collect_profile(Ctx *c) {
     int which = (int)((i / 2) % (c->prm.use_tvb ? 2 : 1));
     c->prof_ms[which] += ms;
   }
-  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   c->ev.clear();
+  c->evnext = 0;
+}
+
+static void clear_graphs(Ctx *c) {
+  for (auto &g : c->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+}
+
+// MRAB bookkeeping after an update of level l at tick t (shared by the eager and the graph paths)
+static void commit_update(Ctx *c, int l, long t, const StepParams &p) {
+  c->n_updates += p.k1 - p.k0;
+  c->par[l] ^= 1;
+  c->kcount[l] = c->kcount[l] + 1;
+  c->tick_s[l] = t;
+  c->t_e[l] = t + (1L << (l - 1));
+}
+
+// One macro step of a single-rank context through a cached CUDA graph: the parameters of every
+// update are computed first (with the bookkeeping); an identical sequence replays its graph,
+// a new one is captured (up to kMaxGraphs) and launched.
+constexpr size_t kMaxGraphs = 12;
+
+// parameters of the next macro step, with its bookkeeping applied to c
+static std::vector<StepParams> next_step_params(Ctx *c) {
+  std::vector<StepParams> seq;
+  seq.reserve(c->schedule.size());
+  for (auto &st : c->schedule) {
+    const long t = c->tick + st.second;
+    seq.push_back(update_params(c, st.first, t));
+    commit_update(c, st.first, t, seq.back());
+  }
+  return seq;
+}
+
+static Ctx::StepGraph *find_graph(Ctx *c, const std::vector<StepParams> &seq) {
+  for (auto &g : c->graphs)
+    if (g.seq.size() == seq.size() && std::memcmp(g.seq.data(), seq.data(), sizeof(StepParams) * seq.size()) == 0)
+      return &g;
+  return nullptr;
+}
+
+static int capture_graph(Ctx *c, std::vector<StepParams> seq) {
+  CK(cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeThreadLocal));
+  for (const StepParams &p : seq) {
+    if (p.k1 > p.k0) {
+      launch(0, false, c->N, p, c->gstream, c->f32);
+      if (c->prm.use_tvb) launch(1, false, c->N, p, c->gstream, c->f32);
+    }
+  }
+  cudaGraph_t graph = nullptr;
+  const cudaError_t le = cudaGetLastError();
+  const cudaError_t ee = cudaStreamEndCapture(c->gstream, &graph);  // always ends the capture
+  if (le != cudaSuccess || ee != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    return cuda_fail(c, le != cudaSuccess ? le : ee, "graph capture");
+  }
+  Ctx::StepGraph g;
+  g.seq = std::move(seq);
+  cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
+  c->graphs.push_back(std::move(g));
+  return SWE_OK;
+}
+
+static bool ramp_done(const Ctx *c) {
+  for (int l = 1; l <= c->L; l++)
+    if (c->off[l] > c->off[l - 1] && c->kcount[l] < 2) return false;
+  return true;
+}
+
+static int graph_step(Ctx *c) {
+  if (!c->gstream) {
+    CK(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->gev1, cudaEventDisableTiming));
+  }
+  const bool after_ramp = ramp_done(c);
+  std::vector<StepParams> seq = next_step_params(c);
+  c->cur = seq.back();
+  Ctx::StepGraph *g = find_graph(c, seq);
+  if (!g) {
+    if (c->graphs.size() >= kMaxGraphs) {  // cache full: launch eagerly
+      for (const StepParams &p : seq)
+        if (p.k1 > p.k0) {
+          launch(0, false, c->N, p, c->stream, c->f32);
+          if (c->prm.use_tvb) launch(1, false, c->N, p, c->stream, c->f32);
+        }
+      return SWE_OK;
+    }
+    if (int rc = capture_graph(c, seq)) return rc;
+    g = &c->graphs.back();
+    if (after_ramp) {
+      // the launch sequence is periodic (ring slot mod 3, parity mod 2): capture the next five
+      // phases now, on a copy of the bookkeeping, so that later steps only replay
+      const int par[9] = {c->par[0], c->par[1], c->par[2], c->par[3], c->par[4], c->par[5], c->par[6], c->par[7],
+                          c->par[8]};
+      int kc[9];
+      long ts[9], te[9];
+      for (int l = 0; l <= 8; l++) kc[l] = c->kcount[l], ts[l] = c->tick_s[l], te[l] = c->t_e[l];
+      const long tick = c->tick, nup = c->n_updates;
+      for (int k = 0; k < 5 && c->graphs.size() < kMaxGraphs; k++) {
+        c->tick += 1L << (c->L - 1);
+        std::vector<StepParams> s2 = next_step_params(c);
+        if (!find_graph(c, s2))
+          if (int rc = capture_graph(c, std::move(s2))) return rc;
+      }
+      for (int l = 0; l <= 8; l++) c->par[l] = par[l], c->kcount[l] = kc[l], c->tick_s[l] = ts[l], c->t_e[l] = te[l];
+      c->tick = tick;
+      c->n_updates = nup;
+      g = find_graph(c, seq);
+    }
+  }
+  CK(cudaEventRecord(c->gev0, c->stream));  // the step starts after the caller's prior work
+  CK(cudaStreamWaitEvent(c->gstream, c->gev0, 0));
+  CK(cudaGraphLaunch(g->exec, c->gstream));
+  CK(cudaEventRecord(c->gev1, c->gstream));  // and the caller's later work waits for the step
+  CK(cudaStreamWaitEvent(c->stream, c->gev1, 0));
+  return SWE_OK;
 }
 
 // One MRAB update of level l at tick t for every context of the group, with
@@ -992,13 +1129,7 @@ static int group_update(std::vector<Ctx *> &G, int l, long t) {
     if (int rc = xtransfer(c, 1, l)) return rc;
   for (Ctx *c : G)
     if (int rc = xunpack(c, 1, l, c->cur.write_par, c->cur.write_slot)) return rc;
-  for (Ctx *c : G) {
-    c->n_updates += c->cur.k1 - c->cur.k0;
-    c->par[l] ^= 1;
-    c->kcount[l] = c->kcount[l] + 1;
-    c->tick_s[l] = t;
-    c->t_e[l] = t + (1L << (l - 1));
-  }
+  for (Ctx *c : G) commit_update(c, l, t, c->cur);
   return SWE_OK;
 }
 
@@ -1093,8 +1224,12 @@ static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
       }
   }
   Ctx *c0 = G[0];
-  for (auto &st : c0->schedule)
-    if (int rc = group_update(G, st.first, c0->tick + st.second)) return rc;
+  if (G.size() == 1 && c0->nranks <= 1 && !c0->prof && c0->use_graphs) {
+    if (int rc = graph_step(c0)) return rc;
+  } else {
+    for (auto &st : c0->schedule)
+      if (int rc = group_update(G, st.first, c0->tick + st.second)) return rc;
+  }
   for (Ctx *c : G) {
     c->tick += 1L << (c->L - 1);
     Ctx *c_ = c;
@@ -1465,6 +1600,11 @@ void swe_destroy(swe_ctx *h) {
                   c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG, c->dOpsGf,
                   c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
                   c->dXrIdx,   c->dDry,   c->dCounters};
+  clear_graphs(c);
+  if (c->gstream) cudaStreamDestroy(c->gstream);
+  if (c->gev0) cudaEventDestroy(c->gev0);
+  if (c->gev1) cudaEventDestroy(c->gev1);
+  for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
   for (void *p : ptrs) c->dfree(p);
   if (c->hCounters) cudaFreeHost(c->hCounters);
   if (c->hInjected) cudaFreeHost(c->hInjected);
