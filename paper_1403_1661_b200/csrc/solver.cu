@@ -409,8 +409,8 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   size_t smem = INIT ? 0 : sizeof(T) * SmemOps<N>::scalar_total;
   int grid = (n + K1_BLOCK - 1) / K1_BLOCK;
 #if K1_PERSIST
-  static int resident = 0;  // one per template instance: SMs x resident blocks per SM
-  if (resident == 0) {
+  int resident = 0;  // SMs x resident blocks per SM (per launch: devices differ)
+  {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -422,11 +422,9 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   if constexpr (!INIT && N >= K1_MMA_MIN_N && sizeof(T) == 8) {  // FP64 tensor path (FP32: scalar path)
     const size_t smem_mma =
         sizeof(double) * (SmemOps<N>::total + (K1_MMA_TILE ? (size_t)(4 * SmemOps<N>::Np + 1) * (K1_BLOCK + kTilePad) : 0));
-    static bool attr = false;
-    if (!attr) {
+    // function attributes are per device: set them on every launch that needs more than the 48 KB default
+    if (smem_mma > 48 * 1024)
       cudaFuncSetAttribute(k_rhs_update_mma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mma);
-      attr = true;
-    }
     k_rhs_update_mma<N><<<(n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem_mma, s>>>(
         reinterpret_cast<const StepParams &>(p));
     return;
