@@ -323,3 +323,11 @@ def test_parity_outflow_boundary():
     dt = si.dt_for(w.mesh, w.N, w.g, 1.0, 0.0, 0.2, u_max=2.0)
     o, s, _ = run_both(w, 150, dt)
     assert_parity(o, s, w.g)
+
+
+def test_parity_outflow_boundary_tensor_path():
+    """The N = 4 tensor-path K1 (k_rhs_update_mma) with a transmissive outflow boundary (A7')."""
+    w = si.c7_rarefaction_outflow(4, 2, True, t0=4.8)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.0, 0.0, 0.2, u_max=2.0)
+    o, s, _ = run_both(w, 80, dt)
+    assert_parity(o, s, w.g)
