@@ -41,6 +41,36 @@ __global__ void k_speeds(int K, int Np, double g, double e4, double a_floor, con
   ae[e] = a_floor > amax ? a_floor : amax;
 }
 
+// Level binning on the device, bit-identical to the host bin_levels_rmin() (reading A19):
+// r_e = Hk_e / a_e (IEEE division; +inf when a_e = 0), r_min = min_e r_e,
+// level_e = 1 + max{k < L : r_e >= 2^k r_min}.  Hk is the host's own array (uploaded once).
+// Positive doubles (and +inf) order like their bit patterns, so r_min is an atomicMin on the bits.
+__global__ void k_rmin(int K, const double *hk, const double *ae, unsigned long long *rmin_bits) {
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double r = inf;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K; e += gridDim.x * blockDim.x) {
+    const double re = ae[e] > 0.0 ? __ddiv_rn(hk[e], ae[e]) : inf;
+    r = re < r ? re : r;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double q = __shfl_xor_sync(0xffffffffu, r, o);
+    r = q < r ? q : r;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMin(rmin_bits, (unsigned long long)__double_as_longlong(r));
+}
+__global__ void k_levels(int K, const double *hk, const double *ae, const double *rmin_p, int L, int32_t *level,
+                         const int32_t *resident, int *changed) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= K) return;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const double r = ae[e] > 0.0 ? __ddiv_rn(hk[e], ae[e]) : inf, rmin = *rmin_p;
+  int l = 1;
+  for (int k = 1; k < L; k++)
+    if (r >= ldexp(rmin, k)) l = k + 1;
+  level[e] = l;
+  if (resident && resident[e] != l) atomicOr(changed, 1);
+}
+
 // caller layout [K][Np] (3 arrays) -> internal [3][Np][K] in internal order
 template <typename T>
 __global__ void k_scatter_state(int K, int Np, const int *orig, const double *h, const double *hu, const double *hv,
@@ -214,6 +244,10 @@ struct Ctx {
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
   double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
   double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dOpsGf = nullptr, *dRmin = nullptr;
+  double *dHk = nullptr;                 // host Hk (caller order), for the device binning
+  int32_t *dLev = nullptr, *dLevRes = nullptr;  // binned levels; levels of the resident layout
+  int *dFlag = nullptr;
+  bool levres_ok = false;  // dLevRes holds the levels of the resident layout
   double *dXsBuf = nullptr, *dXrBuf = nullptr;
   int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
   size_t xcap = 0;  // capacity (entries) of the exchange index/buffer arrays
@@ -1162,31 +1196,43 @@ static int group_init_limit(std::vector<Ctx *> &G) {
 
 // r_min over all ranks (levels are global, reading A19)
 static int group_bin(std::vector<Ctx *> &G, int nlevels) {
+  // r_min on the device, reduced over the group's contexts and over NCCL ranks
   const double inf = std::numeric_limits<double>::infinity();
-  std::vector<std::vector<double>> ae(G.size());
   double rmin = inf;
-  for (size_t i = 0; i < G.size(); i++) {
-    Ctx *c = G[i];
-    ae[i].resize(c->Kin);
-    CK(cudaMemcpyAsync(ae[i].data(), c->dAe, sizeof(double) * c->Kin, cudaMemcpyDeviceToHost, c->stream));
+  for (Ctx *c : G) {
+    const unsigned long long infbits = 0x7ff0000000000000ULL;
+    CK(cudaMemcpyAsync(c->dRmin, &infbits, sizeof(infbits), cudaMemcpyHostToDevice, c->stream));
+    k_rmin<<<std::min((c->Kin + 255) / 256, 4 * 148), 256, 0, c->stream>>>(c->Kin, c->dHk, c->dAe,
+                                                                          (unsigned long long *)c->dRmin);
+    CK(cudaGetLastError());
+    if (G.size() == 1 && c->comm)  // global minimum across NCCL ranks
+      NK(ncclAllReduce(c->dRmin, c->dRmin, 1, ncclDouble, ncclMin, c->comm, c->stream));
+    double r = inf;
+    CK(cudaMemcpyAsync(&r, c->dRmin, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (int e = 0; e < c->Kin; e++) {
-      double r = ae[i][e] > 0.0 ? c->mesh.hk[e] / ae[i][e] : inf;
-      if (r < rmin) rmin = r;
-    }
+    rmin = std::min(rmin, r);
   }
-  if (G.size() == 1 && G[0]->comm) {  // global minimum across NCCL ranks
-    Ctx *c = G[0];
+  for (Ctx *c : G) {
+    // levels on the device; the host needs them only when they differ from the resident layout's
+    const bool cmp = c->layout_valid && c->levres_ok && c->L == nlevels;
+    int changed = 0;
     CK(cudaMemcpyAsync(c->dRmin, &rmin, sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    NK(ncclAllReduce(c->dRmin, c->dRmin, 1, ncclDouble, ncclMin, c->comm, c->stream));
-    CK(cudaMemcpyAsync(&rmin, c->dRmin, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), c->stream));
+    k_levels<<<(c->Kin + 255) / 256, 256, 0, c->stream>>>(c->Kin, c->dHk, c->dAe, c->dRmin, nlevels, c->dLev,
+                                                         cmp ? c->dLevRes : nullptr, c->dFlag);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&changed, c->dFlag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-  }
-  for (size_t i = 0; i < G.size(); i++) {
-    Ctx *c = G[i];
-    std::vector<int32_t> lev(c->Kin, 1);
-    bin_levels_rmin(c->Kin, c->mesh.hk.data(), ae[i].data(), nlevels, rmin, lev.data());
-    if (int rc = materialize(c, lev, nlevels)) return rc;
+    if (cmp && !changed) {  // same levels: keep the layout, scatter the new state
+      if (int rc = materialize(c, c->level, nlevels)) return rc;
+    } else {
+      std::vector<int32_t> lev(c->Kin, 1);
+      CK(cudaMemcpyAsync(lev.data(), c->dLev, sizeof(int32_t) * c->Kin, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (int rc = materialize(c, lev, nlevels)) return rc;
+      CK(cudaMemcpyAsync(c->dLevRes, c->dLev, sizeof(int32_t) * c->Kin, cudaMemcpyDeviceToDevice, c->stream));
+      c->levres_ok = true;
+    }
   }
   return group_init_limit(G);
 }
@@ -1255,6 +1301,7 @@ static int ensure_materialized_group(std::vector<Ctx *> &G) {
   if (!need) return SWE_OK;
   for (Ctx *c : G) {
     std::vector<int32_t> ones(c->Kin, 1);
+    c->levres_ok = false;
     if (int rc = materialize(c, ones, 1)) return rc;
   }
   return group_init_limit(G);
@@ -1414,6 +1461,10 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   if (rc) return fail(rc);
   c->dBcaller = (double *)c->dalloc(sizeof(double) * (size_t)c->Kin * c->Np);
   c->dWm2 = (double *)c->dalloc(sizeof(double) * c->Np);
+  c->dHk = (double *)c->dalloc(sizeof(double) * c->Kin);
+  c->dLev = (int32_t *)c->dalloc(sizeof(int32_t) * c->Kin);
+  c->dLevRes = (int32_t *)c->dalloc(sizeof(int32_t) * c->Kin);
+  c->dFlag = (int *)c->dalloc(sizeof(int));
   std::vector<double> sops = smem_ops_any(c->ops);
   c->dOpsG = (double *)c->dalloc(sizeof(double) * sops.size());
   std::vector<float> sopsf(sops.begin(), sops.end());
@@ -1428,6 +1479,8 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   if (cudaMemcpyAsync(c->dBcaller, B, sizeof(double) * (size_t)c->Kin * c->Np, cudaMemcpyHostToDevice, c->stream) !=
           cudaSuccess ||
       cudaMemcpyAsync(c->dWm2, wm2.data(), sizeof(double) * c->Np, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->dHk, c->mesh.hk.data(), sizeof(double) * c->Kin, cudaMemcpyHostToDevice, c->stream) !=
+          cudaSuccess ||
       cudaMemcpyAsync(c->dOpsG, sops.data(), sizeof(double) * sops.size(), cudaMemcpyHostToDevice, c->stream) !=
           cudaSuccess ||
       cudaMemcpyAsync(c->dOpsGf, sopsf.data(), sizeof(float) * sopsf.size(), cudaMemcpyHostToDevice, c->stream) !=
@@ -1595,7 +1648,7 @@ void swe_destroy(swe_ctx *h) {
         if (p == c) p = nullptr;
     }
   void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo,
-                  c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG, c->dOpsGf,
+                  c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG, c->dOpsGf, c->dHk, c->dLev, c->dLevRes, c->dFlag,
                   c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
                   c->dXrIdx,   c->dDry,   c->dCounters};
   clear_graphs(c);
