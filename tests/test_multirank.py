@@ -143,3 +143,54 @@ def test_partitioned_group_bit_identical(nparts, nlevels):
         assert np.array_equal(merged[f], full[f])  # bit-identical to the single-rank run
     assert max(parity_rel(merged, o.get_state(), w.g)) <= 1e-12
     assert np.array_equal(parts[0].levels(), ref.levels())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_c5_rank_strips_bit_identical(nranks):
+    """bench.py's multi-rank setup without NCCL: every rank builds only its own C5 y-strip plus
+    buffer rows (si.c5_rank_strip: own numbering, owner by centroid, gid = exact centroid key); the
+    ranks run as an in-process group on one GPU.  By global id, their owned elements must equal a
+    single-rank run of the whole basin bit for bit, levels included."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    base_n, N, L = 80, 3, 4
+    full = si.c5_tsunami(P=nranks, base_n=base_n, shuffle_seed=None)
+    mf = full.mesh
+    x, y = P.nodes(mf.vx, mf.vy, mf.etov, N)
+    Bf, hf, huf, hvf = full.fields(x, y)
+    dt = si.dt_for(mf, N, full.g, 4001.0, full.params["a_floor"], full.dt_factor)
+    ref = P.Solver(mf.vx, mf.vy, mf.etov, Bf, N, full.g, params=full.params)
+    ref.set_state(hf, huf, hvf)
+    gid_full = si.centroid_keys(mf, si.C5_LX / base_n)
+    where = {int(g): i for i, g in enumerate(gid_full)}
+    parts, owners, gids = [], [], []
+    for r in range(nranks):
+        w, owner, gid = si.c5_rank_strip(r, nranks, base_n)
+        m = w.mesh
+        xr, yr = P.nodes(m.vx, m.vy, m.etov, N)
+        B, h, hu, hv = w.fields(xr, yr)
+        s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=w.params, rank=r, nranks=nranks, owner=owner, gid=gid)
+        parts.append((s, (h, hu, hv)))
+        owners.append(owner)
+        gids.append(gid)
+    P.link_group([s for s, _ in parts])
+    for s, st in parts:
+        s.set_state(*st)
+    for _ in range(3):
+        ref.step(dt, L)
+        P.step_group([s for s, _ in parts], dt, L)
+    fs = ref.get_state()
+    flev = ref.levels()
+    covered = 0
+    for r, (s, st) in enumerate(parts):
+        out = tuple(np.full_like(st[0], np.nan) for _ in range(3))
+        s.get_state(out)
+        lev = s.levels()
+        own = np.where(owners[r] == r)[0]
+        idx = np.array([where[int(g)] for g in gids[r][own]])
+        for f in range(3):
+            assert np.array_equal(out[f][own], fs[f][idx])
+        assert np.array_equal(lev[own], flev[idx])
+        covered += len(own)
+    assert covered == mf.K
