@@ -71,7 +71,7 @@ __global__ void k_levels(int K, const double *hk, const double *ae, const double
   if (resident && resident[e] != l) atomicOr(changed, 1);
 }
 
-// caller layout [K][Np] (3 arrays) -> internal [3][Np][K] in internal order
+// caller layout [K][Np] (3 arrays) -> internal element-blocked [K/32][3][Np][32] in internal order
 template <typename T>
 __global__ void k_scatter_state(int K, int Np, const int *orig, const double *h, const double *hu, const double *hv,
                                 T *Q) {
@@ -79,9 +79,9 @@ __global__ void k_scatter_state(int K, int Np, const int *orig, const double *h,
   if (k >= K) return;
   size_t e = (size_t)orig[k];
   for (int i = 0; i < Np; i++) {
-    Q[(size_t)i * K + k] = (T)h[e * Np + i];
-    Q[(size_t)(Np + i) * K + k] = (T)hu[e * Np + i];
-    Q[(size_t)(2 * Np + i) * K + k] = (T)hv[e * Np + i];
+    Q[eb_at(k, i, 3 * Np)] = (T)h[e * Np + i];
+    Q[eb_at(k, Np + i, 3 * Np)] = (T)hu[e * Np + i];
+    Q[eb_at(k, 2 * Np + i, 3 * Np)] = (T)hv[e * Np + i];
   }
 }
 
@@ -96,18 +96,19 @@ __global__ void k_geo(int K, const double *V, T *geo) {
   const double xr = 0.5 * (X[1] - X[0]), xs = 0.5 * (X[2] - X[0]), yr = 0.5 * (Y[1] - Y[0]), ys = 0.5 * (Y[2] - Y[0]);
   const double J = xr * ys - xs * yr;
   const double rJ = 1.0 / J;
-  geo[e] = (T)(ys * rJ);
-  geo[K + e] = (T)(-xs * rJ);
-  geo[2 * (size_t)K + e] = (T)(-yr * rJ);
-  geo[3 * (size_t)K + e] = (T)(xr * rJ);
-  geo[4 * (size_t)K + e] = (T)J;
+  T *G = geo + eb_base(e, kGeoRows);  // element-blocked [K/32][14][32]
+  G[0] = (T)(ys * rJ);
+  G[kEB] = (T)(-xs * rJ);
+  G[2 * kEB] = (T)(-yr * rJ);
+  G[3 * kEB] = (T)(xr * rJ);
+  G[4 * kEB] = (T)J;
   for (int f = 0; f < 3; f++) {
     const int f1 = f == 2 ? 0 : f + 1;
     const double dx = X[f1] - X[f], dy = Y[f1] - Y[f];
     const double len = sqrt(dx * dx + dy * dy);
-    geo[(size_t)(5 + 3 * f) * K + e] = (T)(dy / len);
-    geo[(size_t)(6 + 3 * f) * K + e] = (T)(-dx / len);
-    geo[(size_t)(7 + 3 * f) * K + e] = (T)(0.5 * len * rJ);
+    G[(5 + 3 * f) * kEB] = (T)(dy / len);
+    G[(6 + 3 * f) * kEB] = (T)(-dx / len);
+    G[(7 + 3 * f) * kEB] = (T)(0.5 * len * rJ);
   }
 }
 
@@ -142,7 +143,7 @@ __global__ void k_scatter_field(int K, int Np, const int *orig, const double *sr
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   size_t e = (size_t)orig[k];
-  for (int i = 0; i < Np; i++) dst[(size_t)i * K + k] = (T)src[e * Np + i];
+  for (int i = 0; i < Np; i++) dst[eb_at(k, i, Np)] = (T)src[e * Np + i];  // element-blocked [K/32][Np][32]
 }
 
 // internal committed state (parity per level) -> caller layout
@@ -160,12 +161,12 @@ __global__ void k_gather_state(const __grid_constant__ GatherParams p) {
   int c = 0;
   for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
   const size_t K = p.Kstride;
-  const T *Q = (const T *)p.Q + (size_t)p.par[c] * 3 * p.Np * K;
+  const T *Q = (const T *)p.Q + (size_t)p.par[c] * 3 * p.Np * eb_pad(K) + eb_base(k, 3 * p.Np);
   size_t e = (size_t)p.orig[k];
   for (int i = 0; i < p.Np; i++) {
-    p.h[e * p.Np + i] = (double)Q[(size_t)i * K + k];
-    p.hu[e * p.Np + i] = (double)Q[(size_t)(p.Np + i) * K + k];
-    p.hv[e * p.Np + i] = (double)Q[(size_t)(2 * p.Np + i) * K + k];
+    p.h[e * p.Np + i] = (double)Q[(size_t)i * kEB];
+    p.hu[e * p.Np + i] = (double)Q[(size_t)(p.Np + i) * kEB];
+    p.hv[e * p.Np + i] = (double)Q[(size_t)(2 * p.Np + i) * kEB];
   }
 }
 
@@ -180,12 +181,12 @@ __global__ void k_diag(const __grid_constant__ GatherParams p, const double *V, 
     int c = 0;
     for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
     const size_t K = p.Kstride;
-    const T *Q = (const T *)p.Q + (size_t)p.par[c] * 3 * p.Np * K;
+    const T *Q = (const T *)p.Q + (size_t)p.par[c] * 3 * p.Np * eb_pad(K) + eb_base(k, 3 * p.Np);
     double x0 = V[k], x1 = V[K + k], x2 = V[2 * K + k], y0 = V[3 * K + k], y1 = V[4 * K + k], y2 = V[5 * K + k];
     double J = 0.25 * ((x1 - x0) * (y2 - y0) - (x2 - x0) * (y1 - y0));
     double acc = 0.0;
     for (int i = 0; i < p.Np; i++) {
-      double h = (double)Q[(size_t)i * K + k];
+      double h = (double)Q[(size_t)i * kEB];
       acc += wm2[i] * h;
       mn = fmin(mn, h);
     }
@@ -573,15 +574,16 @@ static int alloc_state(Ctx *c) {
   if (c->dQ) return SWE_OK;
   size_t K = c->K, Np = c->Np, Kin = c->Kin;
   const size_t es = c->esz;  // T-typed arrays
-  c->dQ = (double *)c->dalloc(es * 2 * 3 * Np * K);
-  c->dR = (double *)c->dalloc(es * 3 * 3 * Np * K);
-  c->dB = (double *)c->dalloc(es * Np * K);
+  const size_t Kp = eb_pad(K);  // element-blocked arrays: whole blocks of kEB elements
+  c->dQ = (double *)c->dalloc(es * 2 * 3 * Np * Kp);
+  c->dR = (double *)c->dalloc(es * 3 * 3 * Np * Kp);
+  c->dB = (double *)c->dalloc(es * Np * Kp);
   c->dV = (double *)c->dalloc(sizeof(double) * 6 * K);
   c->dMeans = (double *)c->dalloc(es * 3 * K);
   c->dUT = (double *)c->dalloc(es * 9 * K);
   c->dTalpha = (double *)c->dalloc(es * 6 * K);
   c->dTgeo = (double *)c->dalloc(es * 7 * K);
-  c->dGeo = (double *)c->dalloc(es * 14 * K);
+  c->dGeo = (double *)c->dalloc(es * kGeoRows * Kp);
   c->dAe = (double *)c->dalloc(sizeof(double) * Kin);
   c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * Kin);
   c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
