@@ -441,7 +441,7 @@ template <int N, bool INIT, typename T>
 static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
-  size_t smem = INIT ? 0 : sizeof(T) * SmemOps<N>::scalar_total;
+  size_t smem = INIT ? 0 : (size_t)k1_ops_bytes<N, T>();
   int grid = (n + K1_BLOCK - 1) / K1_BLOCK;
 #if K1_PERSIST
   int resident = 0;  // SMs x resident blocks per SM (per launch: devices differ)
