@@ -127,14 +127,14 @@ __global__ void k_tvb_geo(int K, const double *V, T *tgeo) {
     const double dx = XV[(f + 1) % 3] - XV[f], dy = YV[(f + 1) % 3] - YV[f];
     len[f] = sqrt(dx * dx + dy * dy);
   }
-  tgeo[e] = (T)((4.0 * A) / ((len[0] + len[1]) + len[2]));
+  tgeo[eb_at(e, 0, 7)] = (T)((4.0 * A) / ((len[0] + len[1]) + len[2]));  // element-blocked [K/32][7][32]
   const double bx = (XV[0] + XV[1] + XV[2]) / 3.0, by = (YV[0] + YV[1] + YV[2]) / 3.0;
   for (int i = 0; i < 3; i++) {
     const double mx = 0.5 * (XV[i] + XV[(i + 1) % 3]), my = 0.5 * (YV[i] + YV[(i + 1) % 3]);
     const double tx = mx - bx, ty = my - by;
     const double tl = sqrt(tx * tx + ty * ty);
-    tgeo[(size_t)(1 + 2 * i) * K + e] = (T)(tx / tl);
-    tgeo[(size_t)(2 + 2 * i) * K + e] = (T)(ty / tl);
+    tgeo[eb_at(e, 1 + 2 * i, 7)] = (T)(tx / tl);
+    tgeo[eb_at(e, 2 + 2 * i, 7)] = (T)(ty / tl);
   }
 }
 
@@ -579,14 +579,14 @@ static int alloc_state(Ctx *c) {
   c->dR = (double *)c->dalloc(es * 3 * 3 * Np * Kp);
   c->dB = (double *)c->dalloc(es * Np * Kp);
   c->dV = (double *)c->dalloc(sizeof(double) * 6 * K);
-  c->dMeans = (double *)c->dalloc(es * 3 * K);
-  c->dUT = (double *)c->dalloc(es * 9 * K);
-  c->dTalpha = (double *)c->dalloc(es * 6 * K);
-  c->dTgeo = (double *)c->dalloc(es * 7 * K);
+  c->dMeans = (double *)c->dalloc(es * 3 * Kp);
+  c->dUT = (double *)c->dalloc(es * 9 * Kp);
+  c->dTalpha = (double *)c->dalloc(es * 6 * Kp);
+  c->dTgeo = (double *)c->dalloc(es * 7 * Kp);
   c->dGeo = (double *)c->dalloc(es * kGeoRows * Kp);
   c->dAe = (double *)c->dalloc(sizeof(double) * Kin);
   c->dStage = (double *)c->dalloc(sizeof(double) * 3 * Np * Kin);
-  c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * K);
+  c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * Kp);
   c->dTcode = (int *)c->dalloc(sizeof(int) * K);
   c->dOrig = (int *)c->dalloc(sizeof(int) * K);
   c->dDry = (unsigned char *)c->dalloc(K);
@@ -804,8 +804,9 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
       ag += cg[l];
     }
   }
-  std::vector<double> V((size_t)6 * K, 0.0), TA((size_t)6 * K, 0.0);
-  std::vector<int> E2E((size_t)3 * K), TC(K, 0);
+  // E2E and the TVB alphas are element-blocked ([K/32][rows][32], kernels.cuh), V and TC are [rows][K]
+  std::vector<double> V((size_t)6 * K, 0.0), TA((size_t)6 * eb_pad(K), 0.0);
+  std::vector<int> E2E((size_t)3 * eb_pad(K), 0), TC(K, 0);
   for (int k = 0; k < K; k++) {
     int e = c->order[k];
     const int32_t *v = &c->mesh.etov[(size_t)3 * e];
@@ -824,15 +825,15 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
         // boundary faces are self references (n == e, nf == f); a transmissive outflow face (A7')
         // carries neighbour face code 3 instead
         const bool outflow = n == e && nf == f && c->mesh.bc[(size_t)3 * e + f] == 1;
-        E2E[(size_t)f * K + k] = (inv[n] << 2) | (outflow ? 3 : nf);
+        E2E[eb_at(k, f, 3)] = (inv[n] << 2) | (outflow ? 3 : nf);
       } else {
-        E2E[(size_t)f * K + k] = (k << 2) | f;  // ghosts are never launched
+        E2E[eb_at(k, f, 3)] = (k << 2) | f;  // ghosts are never launched
       }
       size_t s = (size_t)3 * e + f;
       code |= (c->tvb.pj[s] & 3) << (4 * f);
       code |= (c->tvb.pk[s] & 3) << (4 * f + 2);
-      TA[(size_t)(2 * f) * K + k] = c->tvb.aj[s];
-      TA[(size_t)(2 * f + 1) * K + k] = c->tvb.ak[s];
+      TA[eb_at(k, 2 * f, 6)] = c->tvb.aj[s];
+      TA[eb_at(k, 2 * f + 1, 6)] = c->tvb.ak[s];
     }
     TC[k] = code;
   }
