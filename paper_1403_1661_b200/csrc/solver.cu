@@ -464,12 +464,20 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
         reinterpret_cast<const StepParams &>(p));
     return;
   }
+#if K1_CARVEOUT >= 0
+  // shared-memory carveout hint (percent of the maximum): the blocks need ~17 KB per SM, the rest is L1 for the
+  // own-state re-reads and the neighbour gathers
+  cudaFuncSetAttribute(k_rhs_update<N, INIT, T>, cudaFuncAttributePreferredSharedMemoryCarveout, K1_CARVEOUT);
+#endif
   k_rhs_update<N, INIT, T><<<grid, K1_BLOCK, smem, s>>>(p);
 }
 template <int N, typename T>
 static void launch_k2(const StepParamsT<T> &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
+#if K2_CARVEOUT >= 0
+  cudaFuncSetAttribute(k_tvb<N, T>, cudaFuncAttributePreferredSharedMemoryCarveout, K2_CARVEOUT);
+#endif
   k_tvb<N, T><<<(n + 127) / 128, 128, 0, s>>>(p);
 }
 template <typename T>
