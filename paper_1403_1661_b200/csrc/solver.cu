@@ -478,7 +478,7 @@ static void launch_k2(const StepParamsT<T> &p, cudaStream_t s) {
 #if K2_CARVEOUT >= 0
   cudaFuncSetAttribute(k_tvb<N, T>, cudaFuncAttributePreferredSharedMemoryCarveout, K2_CARVEOUT);
 #endif
-  k_tvb<N, T><<<(n + 127) / 128, 128, 0, s>>>(p);
+  k_tvb<N, T><<<(n + K2_BLOCK - 1) / K2_BLOCK, K2_BLOCK, 0, s>>>(p);
 }
 template <typename T>
 static void launch_t(int which, bool init, int N, const StepParamsT<T> &p, cudaStream_t s) {
