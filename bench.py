@@ -14,6 +14,7 @@ Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle
 from __future__ import annotations
 
 import argparse
+import atexit
 import json
 import math
 import os
@@ -45,8 +46,9 @@ class ClockSampler:
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.rows = []
+        self.rows = []  # (host time, fields)
         self.proc = None
+        self.window = None  # host-time window of the timed region
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -54,7 +56,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                          "-lms", os.environ.get("BENCH_CLK_MS", "25")], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -65,7 +67,7 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
 
     def __exit__(self, *a):
         if self.proc:
@@ -76,14 +78,23 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        """Samples taken inside the timed region; if the region is shorter than nvidia-smi's sampling
+        interval, the samples of the warm-up steps just before it (same kernels, GPU busy) are used and
+        the window says so."""
+        rows, window = [], "timed"
+        if self.window:
+            t0, t1, tw = self.window
+            rows = [r for t, r in self.rows if t0 <= t <= t1]
+            if not rows:
+                rows, window = [r for t, r in self.rows if tw <= t <= t1], "warmup+timed"
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "window": window}
 
 
 def workload(P_strip: int, base_n: int, strip: int = 1):
@@ -228,6 +239,10 @@ def main():
         dt = float(tdt.item())
     s.set_state(h, hu, hv)
     stream = torch.cuda.current_stream()
+    clk = ClockSampler(local).__enter__()  # started early: nvidia-smi needs a moment before its first row
+    atexit.register(clk.__exit__, None, None, None)  # no stray nvidia-smi if the run fails below
+    time.sleep(0.5)
+    t_warm = time.time()
     for _ in range(args.warmup):
         s.step(dt, L)
     lev_all = s.levels()
@@ -240,12 +255,15 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            s.step(dt, L)  # single rank: each macro step replays a captured CUDA graph
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    t0 = time.time()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        s.step(dt, L)  # single rank: each macro step replays a captured CUDA graph
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk.window = (t0, time.time(), t_warm)
+    time.sleep(0.05)  # let the reader thread take the last rows of the window
+    clk.__exit__(None, None, None)
     ms = ev0.elapsed_time(ev1)
     # per-kernel device times (K1 / K2 events on the solver stream) from a second, profiled run of the
     # same length (profiling launches eagerly, so it is kept out of the timed region above)
