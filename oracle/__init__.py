@@ -53,6 +53,7 @@ class OrcInfo(C.Structure):
         ("t", C.c_double), ("mass", C.c_double), ("injected_mass", C.c_double), ("min_h", C.c_double),
         ("n_pp", C.c_long), ("n_dry", C.c_long), ("n_tvb", C.c_long),
         ("K", C.c_int), ("Np", C.c_int), ("nlevels", C.c_int), ("level_count", C.c_int * 16),
+        ("n_posfix", C.c_long), ("n_tvb_cw", C.c_long), ("n_adopted", C.c_long), ("n_mismatch", C.c_long),
     ]
 
 
@@ -93,6 +94,8 @@ def lib():
         L.orc_set_threads.argtypes = [C.c_int]
         L.orc_regroup.argtypes = [C.c_void_p]
         L.orc_set_boundary.argtypes = [C.c_void_p, C.c_void_p]
+        L.orc_set_replay.argtypes = [C.c_void_p, C.c_void_p, C.c_long]
+        L.orc_set_replay.restype = C.c_int
         L.orc_toy_mrab.argtypes = [C.c_int, dp, ip, dp, C.c_double, C.c_int, C.c_int, dp, dp, dp, C.c_int]
         _lib = L
     return _lib
@@ -199,6 +202,14 @@ class Oracle:
         if rc:
             raise RuntimeError(rc)
 
+    def set_replay(self, log):
+        """Decision replay: `log` = uint8 [nrec, K] limiter decisions of the product path
+        (one record per limiter application, caller element order).  Takes effect from the next
+        set_state; where this oracle's own decision lies within 1e-9 (relative) of its threshold it
+        adopts the logged one (info()['n_adopted']), larger disagreements count in info()['n_mismatch']."""
+        self._replay = np.ascontiguousarray(log, dtype=np.uint8).reshape(-1, self.K)
+        lib().orc_set_replay(self._h, self._replay.ctypes.data_as(C.c_void_p), self._replay.shape[0])
+
     def step(self, dt, nlevels=1):
         return lib().orc_step(self._h, float(dt), int(nlevels))
 
@@ -270,7 +281,9 @@ class Oracle:
         lib().orc_get_info(self._h, C.byref(inf))
         return {"t": inf.t, "mass": inf.mass, "injected_mass": inf.injected_mass, "min_h": inf.min_h,
                 "n_pp": inf.n_pp, "n_dry": inf.n_dry, "n_tvb": inf.n_tvb, "K": inf.K, "Np": inf.Np,
-                "nlevels": inf.nlevels, "level_count": list(inf.level_count)}
+                "nlevels": inf.nlevels, "level_count": list(inf.level_count),
+                "n_posfix": inf.n_posfix, "n_tvb_cw": inf.n_tvb_cw,
+                "n_adopted": inf.n_adopted, "n_mismatch": inf.n_mismatch}
 
 
 # ---------------------------------------------------------------- small pure functions (pins)
@@ -286,6 +299,7 @@ def _setup_pure(L):
     L.orc_mbar.argtypes = [C.c_double, C.c_double, C.c_double, dp]
     L.orc_rebalance.argtypes = [dp, dp]
     L.orc_posfix.argtypes = [dp, C.c_double, C.c_double, dp]
+    L.orc_posfix.restype = C.c_int
     L.orc_char.argtypes = [C.c_double] * 6 + [dp, dp]
     L._pure_ready = True
 

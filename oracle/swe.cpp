@@ -47,6 +47,8 @@ struct Swe {
   std::vector<TvbEdge> tvb;  // K*3
   Mat M1inv;                 // inverse P1 Gram matrix on the reference triangle
   long n_pp = 0, n_dry = 0, n_tvb = 0;
+  long n_posfix = 0;  // Eq. modified_TVB applications (min vertex of the TVB-limited h below h0)
+  long n_tvb_cw = 0;  // TVB replacements in the component-wise branch (mean depth below h_char, A14)
   double injected = 0;
   std::string err;
 
@@ -56,9 +58,18 @@ struct Swe {
   void rhs(int e, const std::function<void(int, double *)> &nbr, const double *q, double *R) const;
   void means(const double *q, double qb[3]) const;
   void p1_coeffs(const double *qf, double d[3]) const;
-  void pp(int e, double *q);
-  void tvb_apply(const std::vector<int> &E);
+  void pp(int e, double *q, const unsigned char *rec);
+  void tvb_apply(const std::vector<int> &E, const unsigned char *rec);
   void limit(const std::vector<int> &E);
+  // Decision replay: a log of the product path's limiter decisions, one record of K bytes per
+  // limiter application (Alg. 2 line 1, then every level update), element order of the caller; bits
+  // 1 Alg. 3 triggered, 2 dry branch, 4 TVB replaced, 8 Eq. modified_TVB applied, 0xFF not updated.  Where
+  // this oracle's own decision sits within kReplayMargin (relative) of its threshold, it adopts the
+  // logged decision (n_adopted); a disagreement farther from the threshold is counted in n_mismatch.
+  std::vector<unsigned char> replay;
+  long replay_n = 0, replay_u = 0;
+  long n_adopted = 0, n_mismatch = 0;
+  bool decide(bool own, double margin, const unsigned char *rec, int e, unsigned bit);
   void build_tvb_geometry();
   void bin_levels(int L, std::vector<int> &lev) const;
 };
@@ -244,6 +255,23 @@ void Swe::p1_coeffs(const double *qf, double d[3]) const {
   for (int a = 0; a < 3; a++) d[a] = M1inv(a, 0) * rhs[0] + M1inv(a, 1) * rhs[1] + M1inv(a, 2) * rhs[2];
 }
 
+// Decision of a discontinuous branch (A26 replay): own = this oracle's decision, margin = its signed
+// distance to the threshold relative to the threshold's scale.  Without a replay log: own.
+static const double kReplayMargin = 1e-9;
+bool Swe::decide(bool own, double margin, const unsigned char *rec, int e, unsigned bit) {
+  if (!rec || rec[e] == 0xFF) return own;
+  const bool logged = (rec[e] & bit) != 0;
+  if (logged == own) return own;
+  if (std::fabs(margin) < kReplayMargin) {
+#pragma omp atomic
+    n_adopted++;
+    return logged;
+  }
+#pragma omp atomic
+  n_mismatch++;
+  return own;
+}
+
 // Alg. 3, reading O10 / A10-A13.
 // Reading A11': both comparisons of Alg. 3 use a relative tie band tau = 1e-10,
 //   trigger  <=>  h_min <= eps (1 + tau),   dry  <=>  hbar < h0 (1 + tau).
@@ -252,10 +280,11 @@ void Swe::p1_coeffs(const double *qf, double d[3]) const {
 // last bit of the cell mean (measured: the GPU and this oracle disagree on
 // 666 of 2458 triggers in the first Thacker step).
 static const double kTieBand = 1e-10;
-void Swe::pp(int e, double *q) {
+void Swe::pp(int e, double *q, const unsigned char *rec) {
   double hmin = q[0];
   for (int i = 1; i < Np; i++) hmin = std::min(hmin, q[i]);
-  if (hmin > prm.eps * (1.0 + kTieBand)) {
+  const double trig_at = prm.eps * (1.0 + kTieBand);
+  if (!decide(!(hmin > trig_at), (trig_at - hmin) / trig_at, rec, e, 1)) {
     dry[e] = 0;
     return;
   }
@@ -265,7 +294,8 @@ void Swe::pp(int e, double *q) {
   for (int k = 0; k < 3; k++) p1_coeffs(q + k * Np, d[k]);
 #pragma omp atomic
   n_pp++;
-  if (qb[0] < prm.h0 * (1.0 + kTieBand)) {  // dry element: h = h0, hu = hv = 0 (not conservative, A13)
+  const double dry_at = prm.h0 * (1.0 + kTieBand);
+  if (decide(qb[0] < dry_at, (dry_at - qb[0]) / dry_at, rec, e, 2)) {  // dry element: h = h0, hu = hv = 0 (not conservative, A13)
     for (int i = 0; i < Np; i++) {
       q[i] = prm.h0;
       q[Np + i] = 0.0;
@@ -414,18 +444,23 @@ static void rebalance(const double D[3], double Dh[3]) {
 // vertex).  If the smallest is below h0:
 //   theta = clamp((hb + Dbar - h0) / (Dbar - min(-D_i + D_j + D_k)), 0, 1),
 //   Dt_i = Dbar + theta (D_i - Dbar),  Dbar = avg(D).
-static void posfix(const double D[3], double hb, double h0, double out[3]) {
+// fire: < 0 decide by the formula (smallest vertex below h0), 0 / 1 forced (decision replay, A26);
+// margin (optional): (smallest vertex - h0) / h0.
+static bool posfix(const double D[3], double hb, double h0, double out[3], int force = -1, double *margin = nullptr) {
   double Dbar = (D[0] + D[1] + D[2]) / 3.0;
   double combo_min = std::numeric_limits<double>::infinity();
   for (int i = 0; i < 3; i++) combo_min = std::min(combo_min, -D[i] + D[(i + 1) % 3] + D[(i + 2) % 3]);
   double o[3] = {D[0], D[1], D[2]};
-  if (hb + combo_min < h0) {
+  if (margin) *margin = (hb + combo_min - h0) / h0;
+  const bool fire = force < 0 ? hb + combo_min < h0 : force == 1;
+  if (fire) {
     double den = Dbar - combo_min;
     double th = den > 0.0 ? (hb + Dbar - h0) / den : 0.0;
     th = std::min(1.0, std::max(0.0, th));
     for (int i = 0; i < 3; i++) o[i] = Dbar + th * (D[i] - Dbar);
   }
   for (int i = 0; i < 3; i++) out[i] = o[i];
+  return fire;
 }
 
 // Eigenvectors of the normal flux Jacobian along n at the mean state (h, u, v),
@@ -450,13 +485,13 @@ static void char_matrices(double g, double h, double u, double v, double nx, dou
 // TVB (reading O11/A14-A16/A20) on the elements E, using the
 // cell means of the current state of every element (same-level neighbours are
 // post-PP values of this update).
-void Swe::tvb_apply(const std::vector<int> &E) {
+void Swe::tvb_apply(const std::vector<int> &E, const unsigned char *rec) {
   if (!prm.use_tvb) return;
   const int ndof = 3 * Np;
   std::vector<double> mean(3 * (size_t)K);
   for (int e = 0; e < K; e++) means(&mr.Q[(size_t)e * ndof], &mean[3 * (size_t)e]);
   std::vector<double> out(E.size() * (size_t)ndof);
-  std::vector<char> changed(E.size(), 0);
+  std::vector<char> changed(E.size(), 0), fixed(E.size(), 0), cw(E.size(), 0);
   const double h_char = prm.h_char;
   const double mref[3][2] = {{0.0, -1.0}, {0.0, 0.0}, {-1.0, 0.0}};  // reference edge midpoints
 #pragma omp parallel for schedule(dynamic, 64)
@@ -513,10 +548,20 @@ void Swe::tvb_apply(const std::vector<int> &E) {
         if (!mbar(wa[a], wb[a], thr, &lim[a])) all_first = false;
       for (int k = 0; k < 3; k++) Delta[k][i] = Rm[k][0] * lim[0] + Rm[k][1] * lim[1] + Rm[k][2] * lim[2];
     }
+    if (rec && rec[e] != 0xFF && ((rec[e] & 4) != 0) == all_first) {  // TVB decision differs from the log
+#pragma omp atomic
+      n_mismatch++;
+    }
     if (all_first) continue;  // P1 part unchanged: keep the full P^N polynomial
     double Dh[3][3];
     for (int k = 0; k < 3; k++) rebalance(Delta[k], Dh[k]);
-    posfix(Dh[0], hb, prm.h0, Dh[0]);
+    {
+      double D0[3] = {Dh[0][0], Dh[0][1], Dh[0][2]}, mg = 0.0, tmp[3];
+      const bool own = posfix(D0, hb, prm.h0, tmp, -1, &mg);
+      const bool fire = decide(own, mg, rec, e, 8);
+      fixed[idx] = posfix(D0, hb, prm.h0, Dh[0], fire ? 1 : 0) ? 1 : 0;
+    }
+    cw[idx] = hb < h_char ? 1 : 0;
     // replace by the limited P1 function q = qb + sum_i D_i phi_i, phi_i = 1 - 2 lambda_{(i+2)%3}
     double *o = &out[(size_t)idx * ndof];
     for (int nd = 0; nd < Np; nd++) {
@@ -533,17 +578,21 @@ void Swe::tvb_apply(const std::vector<int> &E) {
     if (changed[idx]) {
       std::memcpy(&mr.Q[(size_t)E[idx] * ndof], &out[idx * ndof], sizeof(double) * ndof);
       n_tvb++;
+      n_posfix += fixed[idx];
+      n_tvb_cw += cw[idx];
     }
 }
 
 // Lambda Pi M Pi (Alg. 2 line 5) on the elements E.
 void Swe::limit(const std::vector<int> &E) {
   const int ndof = 3 * Np;
+  const unsigned char *rec = replay_u < replay_n ? &replay[(size_t)replay_u * K] : nullptr;
+  replay_u++;
   if (prm.use_pp) {
 #pragma omp parallel for schedule(dynamic, 64)
-    for (long idx = 0; idx < (long)E.size(); idx++) pp(E[idx], &mr.Q[(size_t)E[idx] * ndof]);
+    for (long idx = 0; idx < (long)E.size(); idx++) pp(E[idx], &mr.Q[(size_t)E[idx] * ndof], rec);
   }
-  tvb_apply(E);
+  tvb_apply(E, rec);
 }
 
 // Level binning (reading A19): from the unlimited state passed to set_state.
@@ -591,6 +640,8 @@ typedef struct {
   long n_pp, n_dry, n_tvb;
   int K, Np, nlevels;
   int level_count[16];
+  long n_posfix, n_tvb_cw;
+  long n_adopted, n_mismatch;
 } orc_info;
 
 int orc_set_threads(int n) {
@@ -729,7 +780,8 @@ int orc_set_state(void *hnd, const double *h, const double *hu, const double *hv
   s->mr.init(K, 3 * Np, 1, 0.0, lev);
   s->mr.Q = s->Q0;
   s->dry.assign(K, 0);
-  s->n_pp = s->n_dry = s->n_tvb = 0;
+  s->n_pp = s->n_dry = s->n_tvb = s->n_posfix = s->n_tvb_cw = 0;
+  s->replay_u = 0;
   s->injected = 0;
   s->have_state = true;
   s->scheduled = false;
@@ -936,6 +988,10 @@ int orc_get_info(void *hnd, orc_info *info) {
   info->n_pp = s->n_pp;
   info->n_dry = s->n_dry;
   info->n_tvb = s->n_tvb;
+  info->n_posfix = s->n_posfix;
+  info->n_tvb_cw = s->n_tvb_cw;
+  info->n_adopted = s->n_adopted;
+  info->n_mismatch = s->n_mismatch;
   return 0;
 }
 
@@ -952,9 +1008,20 @@ void orc_flux(double g, double eps_u, const double *qm, double bm, const double 
   s.prm.eps_u = eps_u;
   s.flux(qm[0], qm[1], qm[2], bm, qp[0], qp[1], qp[2], bp, nx, ny, out);
 }
+// Decision replay: log of nrec records of K bytes (see Swe::replay), consumed one record per
+// limiter application from the next orc_set_state on.  nrec = 0 switches replay off.
+int orc_set_replay(void *hnd, const unsigned char *log, long nrec) {
+  Swe *s = (Swe *)hnd;
+  s->replay.assign(log, log + (size_t)nrec * s->K);
+  s->replay_n = nrec;
+  s->replay_u = 0;
+  s->n_adopted = s->n_mismatch = 0;
+  return 0;
+}
+
 int orc_mbar(double a, double b, double thr, double *out) { return mbar(a, b, thr, out) ? 1 : 0; }
 void orc_rebalance(const double *D, double *out) { rebalance(D, out); }
-void orc_posfix(const double *D, double hb, double h0, double *out) { posfix(D, hb, h0, out); }
+int orc_posfix(const double *D, double hb, double h0, double *out) { return posfix(D, hb, h0, out) ? 1 : 0; }
 void orc_char(double g, double h, double u, double v, double nx, double ny, double *L, double *R) {
   double Lm[3][3], Rm[3][3];
   char_matrices(g, h, u, v, nx, ny, 0.0, Lm, Rm);

@@ -204,7 +204,44 @@ def test_thacker_mass_positivity_accuracy():
     h, hu, hv = o.get_state()
     he, _, _ = ex(d["x"], d["y"], nsteps * dt)
     assert np.abs(h - he).max() < 0.05 * he.max()
-    assert np.abs(o.get_state()[0][:, 0] * 0 + GOLDEN["thacker_h_origin"]["h"] - ex(0.0, 0.0, 0.0)[0]).max() < 1e-12
+
+
+def test_thacker_initial_state_at_the_origin():
+    """Alg. 2 line 1 leaves the smooth wet interior of the bowl untouched: the oracle's
+    limited initial depth at the node sitting on the origin is Eq. pb_exact's 1/(X+Y) (golden)."""
+    w = si.c3_thacker(N=2, n=40)
+    o, d = make_oracle(w)
+    o.set_state(d["h"], d["hu"], d["hv"])
+    at0 = (np.abs(d["x"]) < 1e-9) & (np.abs(d["y"]) < 1e-9)
+    assert at0.sum() >= 1
+    assert np.abs(o.get_state()[0][at0] - GOLDEN["thacker_h_origin"]["h"]).max() < 1e-12
+
+
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_thacker_global_error_rate(N):
+    """on the parabolic bowl the global L2 error of the height converges like O(H^1.5) for
+    N = 1, 2, 3 (the front is continuous but not C^1), while away from the front it is faster.
+    Meshes 2 x n x n, n = 16, 32, 64 (H = 500, 250, 125 m), to t = T/4 (T = 2 pi / omega).
+    Measured: global rates 1.37/1.68 (N=1), 1.29/1.51 (N=2), 1.23/1.47 (N=3)."""
+    import math
+    from tests.test_oracle_verification import _l2
+    ex, om = si.thacker_exact()
+    t_end = 0.25 * 2 * math.pi / om
+    glob, loc = [], []
+    for n in (16, 32, 64):
+        w = si.c3_thacker(N=N, n=n)
+        o, d = make_oracle(w)
+        o.set_state(d["h"], d["hu"], d["hv"])
+        dt = si.dt_for(w.mesh, w.N, w.g, 1.75, 0.0, 0.2, u_max=0.5)
+        ns = int(math.ceil(t_end / dt))
+        for _ in range(ns):
+            assert o.step(t_end / ns, 1) == 0
+        assert o.info()["min_h"] >= 0.0
+        glob.append(_l2(o, w, t_end))
+        loc.append(_l2(o, w, t_end, region=lambda x, y: x * x + y * y < 1500.0 ** 2))
+    rates = [math.log2(glob[0] / glob[1]), math.log2(glob[1] / glob[2])]
+    assert rates[0] > 1.1 and rates[1] > 1.4, rates
+    assert math.log2(loc[1] / loc[2]) > rates[1] + 0.2
 
 
 def test_oracle_regroup_is_set_state_of_the_current_state():
