@@ -95,6 +95,8 @@ def lib():
         L.orc_regroup.argtypes = [C.c_void_p]
         L.orc_set_boundary.argtypes = [C.c_void_p, C.c_void_p]
         L.orc_set_replay.argtypes = [C.c_void_p, C.c_void_p, C.c_long]
+        L.orc_set_boundary_state.argtypes = [C.c_void_p, dp, dp, dp]
+        L.orc_set_boundary_state.restype = C.c_int
         L.orc_set_replay.restype = C.c_int
         L.orc_toy_mrab.argtypes = [C.c_int, dp, ip, dp, C.c_double, C.c_int, C.c_int, dp, dp, dp, C.c_int]
         _lib = L
@@ -200,7 +202,13 @@ class Oracle:
         h, hu, hv = self._shape(h), self._shape(hu), self._shape(hv)
         rc = lib().orc_set_state(self._h, _p(h), _p(hu), _p(hv))
         if rc:
-            raise RuntimeError(rc)
+            raise RuntimeError(f"orc_set_state failed ({rc})")
+
+    def set_boundary_state(self, h, hu, hv):
+        """Dirichlet boundary data (reading A7''): nodal state whose trace is the ghost on faces whose
+        vertices are both tagged 2 (vbc); its cell mean is their TVB ghost mean."""
+        h, hu, hv = self._shape(h), self._shape(hu), self._shape(hv)
+        lib().orc_set_boundary_state(self._h, _p(h), _p(hu), _p(hv))
 
     def set_replay(self, log):
         """Decision replay: `log` = uint8 [nrec, K] limiter decisions of the product path

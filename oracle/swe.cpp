@@ -37,6 +37,9 @@ struct Swe {
   double g = 9.81;
   int N = 0, Np = 0, K = 0, Ng = 0, Ncub = 0;
   std::vector<double> B;    // K*Np
+  // Dirichlet boundary data (reading A7''): the nodal state [e][field][node] whose trace is the ghost state
+  // on the element's Dirichlet faces (and whose cell mean is their TVB ghost mean); empty = not set
+  std::vector<double> Qbnd;
   std::vector<double> Q0;   // unlimited state as passed to set_state (for binning)
   Mrab mr;                  // holds the state in mr.Q, element-major [e][field][node]
   bool have_state = false, scheduled = false;
@@ -72,6 +75,13 @@ struct Swe {
   bool decide(bool own, double margin, const unsigned char *rec, int e, unsigned bit);
   void build_tvb_geometry();
   void bin_levels(int L, std::vector<int> &lev) const;
+  // Dirichlet faces present but no boundary state given
+  bool missing_bnd() const {
+    if (!Qbnd.empty()) return false;
+    for (signed char t : mesh.bc)
+      if (t == 2) return true;
+    return false;
+  }
 };
 
 // A4: continuous desingularised velocity  u = sqrt2 h+ m / sqrt(h+^4 + max(h+^4, eps_u^4)).
@@ -184,8 +194,9 @@ void Swe::rhs(int e, const std::function<void(int, double *)> &nbr, const double
   for (int f = 0; f < 3; f++) {
     int n = mesh.EToE[3 * (size_t)e + f], nf = mesh.EToF[3 * (size_t)e + f];
     bool bnd = (n == e && nf == f);
-    bool outflow = bnd && !mesh.bc.empty() && mesh.bc[3 * (size_t)e + f] == 1;
-    bool wall = bnd && !outflow;
+    const int tag = bnd && !mesh.bc.empty() ? mesh.bc[3 * (size_t)e + f] : 0;
+    bool outflow = tag == 1, dirichlet = tag == 2;
+    bool wall = bnd && !outflow && !dirichlet;
     double nx = mesh.nx[3 * (size_t)e + f], ny = mesh.ny[3 * (size_t)e + f];
     double scale = mesh.sJ[3 * (size_t)e + f] / J;
     if (!bnd) nbr(n, qn);
@@ -205,6 +216,19 @@ void Swe::rhs(int e, const std::function<void(int, double *)> &nbr, const double
         bp = bm;
         hup = hum;
         hvp = hvm;
+      } else if (dirichlet) {  // Dirichlet ghost (A7''): the trace of the prescribed state, B+ = B-
+        double a[3] = {0, 0, 0};
+        const double *qd = &Qbnd[(size_t)e * 3 * Np];
+        for (int i = 0; i < Np; i++) {
+          double w = re.Ig(gm, i);
+          a[0] += w * qd[i];
+          a[1] += w * qd[Np + i];
+          a[2] += w * qd[2 * Np + i];
+        }
+        hp = a[0];
+        hup = a[1];
+        hvp = a[2];
+        bp = bm;
       } else {  // neighbour's Gauss points run in the opposite direction
         int gpn = nf * Ng + (Ng - 1 - j);
         double a[4] = {0, 0, 0, 0};
@@ -523,8 +547,11 @@ void Swe::tvb_apply(const std::vector<int> &E, const unsigned char *rec) {
       for (int p = 0; p < 2; p++) {
         int f = slots[p];
         int n = mesh.EToE[3 * (size_t)e + f], nf = mesh.EToF[3 * (size_t)e + f];
-        if (n == e && nf == f && !mesh.bc.empty() && mesh.bc[3 * (size_t)e + f] == 1) {  // outflow ghost mean
+        const int tag = (n == e && nf == f && !mesh.bc.empty()) ? mesh.bc[3 * (size_t)e + f] : 0;
+        if (tag == 1) {  // outflow ghost mean
           for (int k = 0; k < 3; k++) nm[p][k] = qb[k];
+        } else if (tag == 2) {  // Dirichlet ghost mean: the cell mean of the prescribed state (A7'')
+          means(&Qbnd[(size_t)e * 3 * Np], nm[p]);
         } else if (n == e && nf == f) {  // wall ghost mean
           double nx = mesh.nx[3 * (size_t)e + f], ny = mesh.ny[3 * (size_t)e + f];
           double mn = qb[1] * nx + qb[2] * ny;
@@ -768,6 +795,7 @@ void *orc_create(int nverts, const double *vx, const double *vy, int K, const in
 // caller layout: h[e*Np + i]; internal: Q[(e*3 + field)*Np + i]
 int orc_set_state(void *hnd, const double *h, const double *hu, const double *hv) {
   Swe *s = (Swe *)hnd;
+  if (s->missing_bnd()) return -4;  // the initial TVB needs the Dirichlet ghost means
   int K = s->K, Np = s->Np;
   s->Q0.assign((size_t)K * 3 * Np, 0.0);
   for (int e = 0; e < K; e++)
@@ -795,7 +823,7 @@ int orc_set_state(void *hnd, const double *h, const double *hu, const double *hv
 
 int orc_step(void *hnd, double dt, int nlevels) {
   Swe *s = (Swe *)hnd;
-  if (!s->have_state) return -4;
+  if (!s->have_state || s->missing_bnd()) return -4;
   if (!(dt > 0) || !std::isfinite(dt) || nlevels < 1 || nlevels > 8) return -1;
   if (!s->scheduled) {
     std::vector<int> lev;
@@ -836,7 +864,22 @@ int orc_set_boundary(void *hnd, const signed char *vbc) {
       const size_t i = 3 * (size_t)e + f;
       if (s->mesh.EToE[i] != e || s->mesh.EToF[i] != f) continue;
       const int a = s->mesh.EToV[3 * (size_t)e + f], b = s->mesh.EToV[3 * (size_t)e + (f + 1) % 3];
-      s->mesh.bc[i] = (vbc[a] == 1 && vbc[b] == 1) ? 1 : 0;
+      // both vertices tagged: the face takes the smaller tag (1 outflow, 2 Dirichlet); otherwise a wall
+      s->mesh.bc[i] = (vbc[a] >= 1 && vbc[b] >= 1) ? (signed char)std::min<int>(std::min<int>(vbc[a], vbc[b]), 2) : 0;
+    }
+  return 0;
+}
+
+// Dirichlet boundary data (reading A7''): caller layout [e*Np + i]; kept until replaced.
+int orc_set_boundary_state(void *hnd, const double *h, const double *hu, const double *hv) {
+  Swe *s = (Swe *)hnd;
+  const int K = s->K, Np = s->Np;
+  s->Qbnd.assign((size_t)K * 3 * Np, 0.0);
+  for (int e = 0; e < K; e++)
+    for (int i = 0; i < Np; i++) {
+      s->Qbnd[((size_t)e * 3 + 0) * Np + i] = h[(size_t)e * Np + i];
+      s->Qbnd[((size_t)e * 3 + 1) * Np + i] = hu[(size_t)e * Np + i];
+      s->Qbnd[((size_t)e * 3 + 2) * Np + i] = hv[(size_t)e * Np + i];
     }
   return 0;
 }
@@ -932,6 +975,7 @@ int orc_nodes(void *hnd, double *x, double *y) {
 // Single-rate RHS of a given (unlimited) state, every neighbour synchronised.
 int orc_rhs(void *hnd, const double *h, const double *hu, const double *hv, double *Rh_, double *Rhu, double *Rhv) {
   Swe *s = (Swe *)hnd;
+  if (s->missing_bnd()) return -4;
   int K = s->K, Np = s->Np;
   std::vector<double> Q((size_t)K * 3 * Np);
   for (int e = 0; e < K; e++)

@@ -200,6 +200,38 @@ def c2_vortex(N: int, n: int, shuffle_seed: int | None = SEED) -> Workload:
                     0.1, 0, ex)
 
 
+def c2_vortex_dirichlet(N: int, n: int, shuffle_seed: int | None = SEED) -> Workload:
+    """The translating vortex in the rectangle [-5, 10] x [-6, 6] with Dirichlet boundaries set to the
+    exact solution (reading A7''): every boundary vertex tagged 2.  2 x (5 n / 4) x n triangles
+    (n divisible by 4), no limiters."""
+    m = structured(5 * n // 4, n, -5.0, 10.0, -6.0, 6.0)
+    on_bnd = (np.abs(m.vx + 5.0) < 1e-12) | (np.abs(m.vx - 10.0) < 1e-12) | (np.abs(np.abs(m.vy) - 6.0) < 1e-12)
+    m.vbc = np.where(on_bnd, 2, 0).astype(np.int8)
+    if shuffle_seed is not None:
+        m = shuffle(m, shuffle_seed)
+    ex = vortex_exact()
+    prm = dict(h0=1e-8, use_pp=0, use_tvb=0)
+    return Workload(f"C2D-n{n}", m, N, 2.0, lambda x, y: np.zeros_like(x), lambda x, y: ex(x, y, 0.0), prm, 1,
+                    0.1, 0, ex)
+
+
+def c2_vortex_graded(N: int, n: int, a: float = 0.6, shuffle_seed: int | None = SEED) -> Workload:
+    """The C2 vortex on a periodic mesh with graded spacing: the vertices of the 2 n^2 periodic square are
+    moved by x -> x + a (L / 2 pi) sin(2 pi (x + 10) / L) (and likewise y), L = 20, which keeps x = +-10
+    fixed (periodic partners still coincide) and makes the spacing vary by (1 + a) / (1 - a) (4x at
+    a = 0.6): three MRAB levels binned from the element sizes (reading A19) on a periodic domain."""
+    m = structured(n, n, -10.0, 10.0, -10.0, 10.0, periodic=True)
+    L = 20.0
+    m.vx = m.vx + a * L / (2 * math.pi) * np.sin(2 * math.pi * (m.vx + 10.0) / L)
+    m.vy = m.vy + a * L / (2 * math.pi) * np.sin(2 * math.pi * (m.vy + 10.0) / L)
+    if shuffle_seed is not None:
+        m = shuffle(m, shuffle_seed)
+    ex = vortex_exact()
+    prm = dict(h0=1e-8, use_pp=0, use_tvb=0)
+    return Workload(f"C2G-n{n}", m, N, 2.0, lambda x, y: np.zeros_like(x), lambda x, y: ex(x, y, 0.0), prm, 1,
+                    0.1, 0, ex)
+
+
 THACKER = dict(alpha=1.6e-7, X=1.0, Y=-0.41884, g=9.81)
 
 

@@ -30,6 +30,9 @@ MUTATIONS = {
                             "theta = std::min(1.0, (qb[0]) / (qb[0] - h1min));"),
     "flux_lambda_one_side": ("  double lam = std::max(std::fabs(unm) + std::sqrt(g * hsm), std::fabs(unp) + std::sqrt(g * hsp));",
                              "  double lam = std::fabs(unm) + std::sqrt(g * hsm);"),
+    "dirichlet_ghost_interior": ("        hp = a[0];\n        hup = a[1];\n        hvp = a[2];\n        bp = bm;",
+                                 "        hp = hm;\n        hup = hum;\n        hvp = hvm;\n        bp = bm;"),
+    "dirichlet_tvb_mean_own": ("          means(&Qbnd[(size_t)e * 3 * Np], nm[p]);", "          for (int k = 0; k < 3; k++) nm[p][k] = qb[k];"),
     "source_sign": ("    double S[3] = {0.0, -g * (hc + bc) * bxc, -g * (hc + bc) * byc};",
                     "    double S[3] = {0.0, g * (hc + bc) * bxc, -g * (hc + bc) * byc};"),
 }
