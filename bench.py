@@ -97,6 +97,55 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "window": window}
 
 
+class GpmDram:
+    """DRAM bandwidth utilisation of the GPU over an interval, from the hardware counters NVML's GPU
+    Performance Monitoring reads (NVML_GPM_METRIC_DRAM_BW_UTIL, Hopper and later): an in-run measurement of
+    the traffic the step really moves, next to the algorithmic byte count."""
+
+    def __init__(self, index: int):
+        self.ok = False
+        try:
+            import pynvml as nv
+            self.nv = nv
+            nv.nvmlInit()
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            if not nv.nvmlGpmQueryDeviceSupport(self.h).isSupportedDevice:
+                return
+            self.s1, self.s2 = nv.nvmlGpmSampleAlloc(), nv.nvmlGpmSampleAlloc()
+            mem_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_MEM)
+            bus = nv.nvmlDeviceGetMemoryBusWidth(self.h)
+            self.theoretical_gbs = 2.0 * mem_mhz * 1e6 * bus / 8 / 1e9  # double data rate
+            self.ok = True
+        except Exception as e:  # no NVML / GPM on this box: reported as unavailable
+            self.err = repr(e)
+
+    def start(self):
+        if self.ok:
+            try:
+                self.nv.nvmlGpmSampleGet(self.h, self.s1)
+            except Exception as e:  # GPM present but not permitted here (e.g. containerised driver)
+                self.ok, self.err = False, repr(e)
+
+    def stop(self):
+        if not self.ok:
+            return None
+        try:
+            nv = self.nv
+            nv.nvmlGpmSampleGet(self.h, self.s2)
+            mg = nv.c_nvmlGpmMetricsGet_t()
+            mg.version = nv.NVML_GPM_METRICS_GET_VERSION
+            mg.numMetrics = 1
+            mg.sample1, mg.sample2 = self.s1, self.s2
+            mg.metrics[0].metricId = nv.NVML_GPM_METRIC_DRAM_BW_UTIL
+            nv.nvmlGpmMetricsGet(mg)
+            if mg.metrics[0].nvmlReturn != 0:
+                return None
+            return float(mg.metrics[0].value)
+        except Exception as e:
+            self.err = repr(e)
+            return None
+
+
 def workload(P_strip: int, base_n: int, strip: int = 1):
     import swe_inputs as si
     return si.c5_tsunami(P=P_strip, base_n=base_n, strip=strip)
@@ -134,9 +183,32 @@ def cpu_baseline(args, seconds_budget=30.0):
         if time.perf_counter() - t0 > seconds_budget * 0.5 or n >= args.cpu_steps:
             break
     el = time.perf_counter() - t0
-    return {"value": U * n / el, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"C5 y-strip 1/{args.cpu_strip} ({m.K} elements, N=3, L={w.nlevels}), {n} macro step(s) after "
-                      f"the first, {el:.1f} s"}
+    out = {"value": U * n / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"C5 y-strip 1/{args.cpu_strip} ({m.K} elements, N=3, L={w.nlevels}), {n} macro step(s) after "
+                     f"the first, {el:.1f} s"}
+    del o
+    # the same oracle on one core, on a 1/32 strip (one macro step after the first)
+    oracle.set_threads(1)
+    try:
+        w1 = workload(1, args.base_n, strip=32)
+        m1 = w1.mesh
+        probe = oracle.Oracle(m1.vx, m1.vy, m1.etov, np.zeros((m1.K, Np)), 3, w1.g, **w1.params)
+        x1, y1 = probe.nodes()
+        del probe
+        B1, h1, hu1, hv1 = w1.fields(x1, y1)
+        o1 = oracle.Oracle(m1.vx, m1.vy, m1.etov, B1, 3, w1.g, **w1.params)
+        o1.set_state(h1, hu1, hv1)
+        dt1 = si.dt_for(m1, 3, w1.g, 4001.0, w1.params["a_floor"], w1.dt_factor)
+        assert o1.step(dt1, w1.nlevels) == 0
+        U1 = dof_per_macro_step(o1.levels(), w1.nlevels, Np)
+        t0 = time.perf_counter()
+        assert o1.step(dt1, w1.nlevels) == 0
+        el1 = time.perf_counter() - t0
+        out["one_core"] = {"value": U1 / el1, "cores": 1,
+                           "sample": f"C5 y-strip 1/32 ({m1.K} elements), 1 macro step after the first, {el1:.1f} s"}
+    finally:
+        oracle.set_threads(cores)
+    return out
 
 
 def run_reference(args, rank, world):
@@ -189,12 +261,37 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="halo exchange for N > 1: CUDA-IPC peer copies (default; also ranks sharing a GPU) or NCCL")
     args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "W >= 3"
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # no launcher: start one process per rank here (same environment contract as torchrun)
+        import socket
+
+        import torch.multiprocessing as mp
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        mp.spawn(_spawned_rank, args=(args, port), nprocs=args.gpus, join=True)
+        return
+    run_rank(args)
+
+
+def _spawned_rank(local, args, port):
+    os.environ.update(RANK=str(local), LOCAL_RANK=str(local), WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    run_rank(args)
+
+
+def run_rank(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    assert args.warmup >= 3 or args.impl == "reference", "W >= 3"
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -205,10 +302,26 @@ def main():
     import paper_1403_1661_b200 as P
     import swe_inputs as si
 
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev = local % ndev  # ranks beyond the device count share GPUs (CUDA-IPC transport only)
+    torch.cuda.set_device(dev)
+    shared = world > ndev
+    backend = "gloo" if shared else "nccl"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+        if shared and args.transport == "nccl":
+            raise SystemExit("bench.py: NCCL cannot run two ranks on one GPU; use --transport ipc")
+    tdev = "cuda" if backend == "nccl" else "cpu"
+
+    def allreduce(x, op):
+        t = torch.tensor([x], device=tdev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=op)
+        return float(t.item())
+
     P.lib()
 
     # ---- workload: C5 tsunami basin.  N=1: the full 2000 km x 2000 km basin.  N>1 (weak scaling):
@@ -217,9 +330,11 @@ def main():
     t_setup = time.time()
     if world > 1:
         w, owner, gid = si.c5_rank_strip(rank, world, args.base_n)
-        idbuf = [P.nccl_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(idbuf, src=0)
-        part = dict(rank=rank, nranks=world, owner=owner, gid=gid, nccl_id=idbuf[0])
+        part = dict(rank=rank, nranks=world, owner=owner, gid=gid)
+        if args.transport == "nccl":
+            idbuf = [P.nccl_unique_id() if rank == 0 else None]
+            torch.distributed.broadcast_object_list(idbuf, src=0)
+            part["nccl_id"] = idbuf[0]
     else:
         w = workload(1, args.base_n)
         owner = None
@@ -230,16 +345,16 @@ def main():
     x, y = P.nodes(m.vx, m.vy, m.etov, N)
     B, h, hu, hv = w.fields(x, y)
     del x, y
-    s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=dict(w.params, precision=args.precision), device=local,
+    s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=dict(w.params, precision=args.precision), device=dev,
                  **part)
+    if world > 1 and args.transport == "ipc":
+        P.ipc_connect(s)
     dt = si.dt_for(m, N, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
     if world > 1:
-        tdt = torch.tensor([dt], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tdt, op=torch.distributed.ReduceOp.MIN)
-        dt = float(tdt.item())
+        dt = allreduce(dt, torch.distributed.ReduceOp.MIN)
     s.set_state(h, hu, hv)
     stream = torch.cuda.current_stream()
-    clk = ClockSampler(local).__enter__()  # started early: nvidia-smi needs a moment before its first row
+    clk = ClockSampler(dev).__enter__()  # started early: nvidia-smi needs a moment before its first row
     atexit.register(clk.__exit__, None, None, None)  # no stray nvidia-smi if the run fails below
     time.sleep(0.5)
     t_warm = time.time()
@@ -254,13 +369,16 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    gpm = GpmDram(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.time()
+    gpm.start()
     ev0.record(stream)
     for _ in range(args.steps):
         s.step(dt, L)  # single rank: each macro step replays a captured CUDA graph
     ev1.record(stream)
     torch.cuda.synchronize()
+    dram_util = gpm.stop()
     clk.window = (t0, time.time(), t_warm)
     time.sleep(0.05)  # let the reader thread take the last rows of the window
     clk.__exit__(None, None, None)
@@ -274,39 +392,57 @@ def main():
     s.profile(False)
     prof = s.profile_read()
     prof_ms = prof["k1_ms"] + prof["k2_ms"]
+    ms_rank = ms
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allreduce(ms, torch.distributed.ReduceOp.MAX)
         torch.distributed.barrier()
     ms_per_step = ms / args.steps
     U_all = U
     if world > 1:
-        tu = torch.tensor([float(U)], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tu)
-        U_all = int(tu.item())
+        U_all = int(allreduce(float(U), torch.distributed.ReduceOp.SUM))
     value = U_all * args.steps / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel (K1), algorithmic bytes / event-timed launch duration
+    # ---- roofline.  Bytes: SURVEY 8(d)'s algorithmic count per element-update, B_alg = esz (6 Np [Q r+w] +
+    # 9 Np [AB ring 2 r + 1 w] + Np [B] + 9 Nfp [neighbour face values] + 3 Nfp [neighbour B] + 6 [vertices]
+    # + 12 [means]) + 16 [indices] -- 1824 B at N = 3 in FP64 -- times the element-updates of the run.
+    # Time: the dominant kernel K1, every launch timed with CUDA events on the solver stream (profiled run of
+    # the same steps), and the whole graph-replayed step.
     peak, peak_kind = load_peaks()
-    k1_gbs = prof["k1_bytes"] / (prof["k1_ms"] / 1e3) / 1e9
+    Nfp = N + 1
+    esz = 8 if args.precision == 64 else 4
+    b_alg = esz * (6 * Np + 9 * Np + Np + 9 * Nfp + 3 * Nfp + 6 + 12) + 16
+    upd = U * args.steps / (3 * Np)  # element-updates of this rank in the timed (and in the profiled) steps
+    k1_gbs = b_alg * upd / (prof["k1_ms"] / 1e3) / 1e9
+    step_gbs = b_alg * upd / (ms_rank / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
             "traffic": None, "kernel": f"k_rhs_update<{N}>", "peak_kind": peak_kind,
-            "k1_share_of_step": prof["k1_ms"] / ms if ms > 0 else None,
-            "k2_share_of_step": prof["k2_ms"] / ms if ms > 0 else None,
-            "profiled_run_kernel_ms": prof_ms}
-    traffic_path = os.path.join(ROOT, "profiles", "r01_k1_traffic.json")
-    if N == 3 and args.precision == 64 and os.path.exists(traffic_path):  # ncu capture (profiles/), not this run
-        try:
+            "bytes_model": "SURVEY 8(d) B_alg per element-update", "algorithmic_bytes_per_elem_update": b_alg,
+            "k1_launch_ms_avg": prof["k1_ms"] / max(1, prof["k1_launches"]),
+            "step_achieved": step_gbs, "step_frac": step_gbs / peak,
+            "k1_share_of_kernel_time": prof["k1_ms"] / prof_ms if prof_ms > 0 else None,
+            "k2_share_of_kernel_time": prof["k2_ms"] / prof_ms if prof_ms > 0 else None,
+            "eager_kernel_ms_over_graph_step_ms": prof_ms / ms_rank if ms_rank > 0 else None,
+            "library_k1_model_bytes_per_elem_update": prof["k1_bytes"] / upd if upd else None}
+    if dram_util is None:
+        roof["dram_measured"] = {"source": "NVML GPM DRAM_BW_UTIL", "unavailable": getattr(gpm, "err", "no GPM")}
+    else:  # measured in this run: hardware DRAM counters over the timed region
+        dram_gbs = dram_util / 100.0 * gpm.theoretical_gbs
+        roof["dram_measured"] = {
+            "source": "NVML GPM DRAM_BW_UTIL over the timed region (whole step, all kernels)",
+            "util_pct_of_theoretical": dram_util, "theoretical_gbs": gpm.theoretical_gbs, "gbs": dram_gbs,
+            "frac_of_measured_peak": dram_gbs / peak,
+            "bytes_per_elem_update": dram_gbs * 1e9 * (ms_rank / 1e3) / upd if upd else None}
+    traffic_path = os.path.join(ROOT, "profiles", "r02_k1_traffic.json")
+    if N == 3 and args.precision == 64 and os.path.exists(traffic_path):
+        try:  # K1's own DRAM bytes per launch: ncu --set full capture committed under profiles/ (not this run)
             tr = json.load(open(traffic_path))
             roof["traffic"] = tr["bytes_per_launch"]
+            roof["traffic_source"] = "ncu dram__bytes_read.sum + dram__bytes_write.sum, " + os.path.relpath(
+                traffic_path, ROOT) + " (one level-4 K1 launch; not measured in this run)"
             roof["traffic_launch_elements"] = tr["elements"]
             roof["traffic_bytes_per_elem_update"] = tr["bytes_per_elem_update"]
         except Exception:
             pass
-    k1_updates = U * args.steps / (3 * Np)  # element updates of this rank (K1 launches)
-    if k1_updates:
-        roof["algorithmic_bytes_per_elem_update"] = prof["k1_bytes"] / k1_updates
 
     info = s.info()
 
@@ -319,8 +455,9 @@ def main():
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
         hh, hhu, hhv = pin(h), pin(hu), pin(hv)
         oh, ohu, ohv = pin(np.zeros_like(h)), pin(np.zeros_like(h)), pin(np.zeros_like(h))
+        s.get_state_into(oh, ohu, ohv)  # untimed warm-up of the read-back path (its one-time device buffer)
         state_bytes = 3 * h.size * 8
-        info_bytes = 2 * 8 * ((len(lev) + 255) // 256) + 8 * 4 * 64 + 8 * 64  # partials + counters + injected
+        info_bytes = 2 * 8 * ((len(lev) + 255) // 256) + 8 * 6 * 64 + 8 * 64  # partials + counters + injected
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s.set_state(hh, hhu, hhv)
@@ -331,9 +468,7 @@ def main():
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([el], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            el = float(t.item())
+            el = allreduce(el, torch.distributed.ReduceOp.MAX)
         k = args.e2e_steps
         e2e = {"value": U_all * k / el, "unit": UNIT,
                "h2d_bytes_per_step": int(state_bytes / k), "d2h_bytes_per_step": int(info_bytes + state_bytes / k),
@@ -352,6 +487,8 @@ def main():
         el2 = time.perf_counter() - t0
         e2e["state_every_step"] = {"value": U_all * k / el2, "d2h_bytes_per_step": int(state_bytes)}
 
+    if world > 1:
+        torch.distributed.barrier()  # every rank is done with the others' exchange blocks
     s.close()
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -364,14 +501,16 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
             "config": {"workload": f"C5 synthetic tsunami basin (SURVEY 8(d)), N={N}, 4 MRAB levels, PP+TVB"
-                                   + (f", {world} y-strips (weak scaling, NCCL halo exchange)" if world > 1 else ""),
+                                   + (f", {world} y-strips (weak scaling, {args.transport} halo exchange)"
+                                      if world > 1 else ""),
+                       "ranks_share_gpus": bool(world > 1 and shared),
                        "K_per_rank": int(len(lev)), "level_counts": [int(c) for c in np.bincount(lev, minlength=L + 1)[1:]],
                        "dof_updates_per_step": U_all, "dt": dt, "l2": "inputs larger than L2 (state+history ~13 GB/rank)",
                        "parallelism": f"element partition x{world}", "setup_s": round(t_setup, 1)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(prof["k1_launches"] + prof["k2_launches"]),
             "clocks": clk.summary(),
-            "counters": {"n_pp": info["n_pp"], "n_dry": info["n_dry"], "n_tvb": info["n_tvb"]},
+            "counters": {k: info[k] for k in ("n_pp", "n_dry", "n_tvb", "n_posfix", "n_tvb_cw")},
         }
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -43,7 +43,7 @@ enum {
   SWE_OK = 0,
   SWE_ERR_ARG = -1,       /* invalid argument (NULL, size, dt <= 0, nlevels out of [1,8]) */
   SWE_ERR_MESH = -2,      /* vertex index out of range, zero-area element, face with > 2 owners */
-  SWE_ERR_ORDER = -3,     /* polynomial order outside the supported range [1, 4] */
+  SWE_ERR_ORDER = -3,     /* polynomial order outside the supported range [1, 5] (order 5 with integration order 10) */
   SWE_ERR_STATE = -4,     /* swe_step / swe_get_state before swe_set_state */
   SWE_ERR_SCHEDULE = -5,  /* (dt, nlevels) differ from the first swe_step after swe_set_state */
   SWE_ERR_NONFINITE = -6, /* NaN/Inf produced; the state is left as computed */
@@ -63,9 +63,10 @@ typedef struct {
   int32_t nelems;
   const int32_t *etov;        /* [nelems*3], 0-based vertex indices */
   const int32_t *vperiodic;   /* [nverts] or NULL */
-  /* Boundary tags [nverts] or NULL (reading A7'): an unmatched face whose two vertices are both
-   * tagged 1 is a transmissive outflow boundary (ghost state = interior trace, TVB ghost mean =
-   * own mean); every other unmatched face is a reflective wall. */
+  /* Boundary tags [nverts] or NULL: an unmatched face whose two vertices are both tagged (>= 1) takes
+   * the smaller tag -- 1: transmissive outflow (reading A7': ghost state = interior trace, TVB ghost
+   * mean = own mean), 2: Dirichlet (reading A7'': swe_set_boundary_state); every other unmatched face
+   * is a reflective wall. */
   const int8_t *vbc;
 } swe_mesh;
 
@@ -110,6 +111,10 @@ typedef struct {
    * printed (levels descending, substeps inner) with every neighbour at its latest committed
    * value (SPEC's reading, first order at level interfaces, kept for comparison). */
   int32_t mrab_coupling;
+  /* Decision log for oracle replay (debug): nonzero => every limiter application (Alg. 2
+   * line 1, then every level update) appends one record of nelems bytes to a host log, read with
+   * swe_get_decisions.  Forces eager launches (no CUDA graphs) and one stream sync per update. */
+  int32_t record_decisions;
 } swe_params;
 
 typedef struct {
@@ -123,6 +128,8 @@ typedef struct {
   int64_t n_updates;     /* element updates (sum over launched levels) */
   int32_t K, Np, N, nlevels, nflipped;
   int32_t level_count[8];
+  int64_t n_posfix;      /* TVB-replaced elements whose h needed Eq. modified_TVB (a P1 vertex below h0) */
+  int64_t n_tvb_cw;      /* TVB-replaced elements limited component-wise (mean depth below h_char, A14) */
 } swe_info;
 
 /* ------------------------------------------------------------ solver */
@@ -131,7 +138,7 @@ typedef struct {
  * Host only (no device needed).  Returns SWE_OK or SWE_ERR_MESH/ORDER/ARG. */
 int swe_nodes(const swe_mesh *mesh, int N, double *x, double *y);
 
-/* Build a solver for order N in [1,4], gravity g > 0, nodal bathymetry B
+/* Build a solver for order N in [1,5], gravity g > 0, nodal bathymetry B
  * ([nelems*Np], P^N per element).  Host builder (reference element, mesh
  * connectivity, geometry) + device upload.  On failure *out = NULL. */
 int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe_params *params,
@@ -153,6 +160,15 @@ int swe_step(swe_ctx *ctx, double dt, int nlevels);
 /* Copy the current state to the host, caller order, [nelems*Np] each. */
 int swe_get_state(swe_ctx *ctx, double *h, double *hu, double *hv);
 
+/* Dirichlet boundary data (reading A7''; P:355 sets "Dirichlet boundary conditions ... to the exact
+ * solution").  A boundary face whose two vertices are both tagged 2 in swe_mesh.vbc is a Dirichlet face:
+ * its ghost state is the trace of the nodal state given here ([nelems*Np] each, caller layout; only the
+ * face nodes of elements with Dirichlet faces are used), with B+ = B-, and its TVB ghost mean is that
+ * state's cell mean.  The data stay until the next call (call it between swe_step calls to follow a
+ * time-dependent boundary; it is held constant during a macro step).  swe_step / swe_get_state return
+ * SWE_ERR_STATE while a mesh with Dirichlet faces has no boundary state. */
+int swe_set_boundary_state(swe_ctx *ctx, const double *h, const double *hu, const double *hv);
+
 /* Level regrouping ("elements can be regrouped after every few time steps"):
  * the current state becomes the state of a fresh swe_set_state -- levels re-binned at the next
  * swe_step (which may use a new dt and nlevels), Alg. 2 line 1 applied to it, AB ramp and counters
@@ -171,7 +187,29 @@ int swe_nccl_unique_id(void *id128);
 int swe_link_group(swe_ctx **ctxs, int n);
 int swe_step_group(swe_ctx **ctxs, int n, double dt, int nlevels);
 
+/* CUDA-IPC transport (NVLink peer memory; also two or more ranks sharing one GPU, where NCCL
+ * refuses to run).  Every rank of an nranks > 1 partition exports its exchange block (a cudaMalloc'ed
+ * header with the exchange flags plus two send slots) and maps every other rank's.  An exchange is then:
+ * pack into the own send slot (exchange count mod 2), cuStreamWriteValue64 of the own flag, and per
+ * neighbour cuStreamWaitValue64 on its flag followed by a device copy of the neighbour's segment straight
+ * out of its send slot (peer reads over NVLink).  r_min for the level binning is reduced over all ranks the
+ * same way.
+ *   swe_ipc_handle: blob = NULL -> *bytes = blob size; else writes this rank's blob (device handle, send
+ *                   layout offsets).  Call on every rank, gather the blobs in rank order (e.g. with
+ *                   torch.distributed.all_gather_object), then
+ *   swe_ipc_open:   blobs = nranks blobs of that size, rank order; maps the peers' blocks and selects the
+ *                   IPC transport for swe_step.  SWE_ERR_MESH if two ranks' halo plans disagree. */
+int swe_ipc_handle(swe_ctx *ctx, void *blob, size_t *bytes);
+int swe_ipc_open(swe_ctx *ctx, const void *blobs);
+
 /* ------------------------------------------------------------ introspection */
+/* Decision log (swe_params.record_decisions): nrec records of nelems bytes, caller element
+ * order, one per limiter application since swe_set_state: bit 1 Alg. 3 triggered, 2 dry branch
+ * (P:206), 4 replaced by the TVB limiter, 8 Eq. modified_TVB applied; 0xFF = element
+ * not updated by that application (other level, or not owned).  log = NULL: *nrec receives the record
+ * count; otherwise min(*nrec, count) records are copied and *nrec is set to that number.
+ * SWE_ERR_STATE if recording is off. */
+int swe_get_decisions(swe_ctx *ctx, uint8_t *log, int64_t *nrec);
 int swe_get_levels(swe_ctx *ctx, int32_t *level);                       /* [nelems], 1..nlevels */
 int swe_get_connectivity(const swe_ctx *ctx, int32_t *etoe, int8_t *etof); /* [nelems*3], boundary = self */
 int swe_get_info(swe_ctx *ctx, swe_info *info);

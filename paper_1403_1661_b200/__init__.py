@@ -25,7 +25,7 @@ EXPORTED = ["swe_nodes", "swe_create", "swe_set_state", "swe_step", "swe_get_sta
             "swe_get_connectivity", "swe_get_info", "swe_last_error", "swe_profile", "swe_profile_read",
             "swe_nccl_unique_id", "swe_link_group", "swe_step_group",
             "swe_host_refel", "swe_host_connectivity", "swe_host_hk", "swe_host_levels", "swe_host_tvb_geometry",
-            "swe_host_halo_plan"]
+            "swe_host_halo_plan", "swe_get_decisions", "swe_ipc_handle", "swe_ipc_open", "swe_set_boundary_state"]
 
 
 class SweError(RuntimeError):
@@ -51,14 +51,15 @@ class SweParams(C.Structure):
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_user", C.c_void_p),
                 ("rank", C.c_int32), ("nranks", C.c_int32), ("owner", C.POINTER(C.c_int32)),
                 ("gid", C.POINTER(C.c_int64)), ("nccl_id", C.c_void_p), ("precision", C.c_int32),
-                ("mrab_coupling", C.c_int32)]
+                ("mrab_coupling", C.c_int32), ("record_decisions", C.c_int32)]
 
 
 class SweInfo(C.Structure):
     _fields_ = [("t", C.c_double), ("mass", C.c_double), ("injected_mass", C.c_double), ("min_h", C.c_double),
                 ("n_pp", C.c_int64), ("n_dry", C.c_int64), ("n_tvb", C.c_int64), ("n_updates", C.c_int64),
                 ("K", C.c_int32), ("Np", C.c_int32), ("N", C.c_int32), ("nlevels", C.c_int32),
-                ("nflipped", C.c_int32), ("level_count", C.c_int32 * 8)]
+                ("nflipped", C.c_int32), ("level_count", C.c_int32 * 8), ("n_posfix", C.c_int64),
+                ("n_tvb_cw", C.c_int64)]
 
 
 _lib = None
@@ -82,6 +83,7 @@ def lib():
         L.swe_create.argtypes = [C.POINTER(SweMesh), dp, C.c_int, C.c_double, C.POINTER(SweParams), C.POINTER(vp)]
         L.swe_set_state.argtypes = [vp, dp, dp, dp]
         L.swe_step.argtypes = [vp, C.c_double, C.c_int]
+        L.swe_set_boundary_state.argtypes = [vp, dp, dp, dp]
         L.swe_regroup.argtypes = [vp]
         L.swe_get_state.argtypes = [vp, dp, dp, dp]
         L.swe_destroy.argtypes = [vp]
@@ -89,6 +91,9 @@ def lib():
         L.swe_get_levels.argtypes = [vp, ip]
         L.swe_get_connectivity.argtypes = [vp, ip, C.POINTER(C.c_int8)]
         L.swe_get_info.argtypes = [vp, C.POINTER(SweInfo)]
+        L.swe_get_decisions.argtypes = [vp, C.c_void_p, C.POINTER(C.c_int64)]
+        L.swe_ipc_handle.argtypes = [vp, C.c_void_p, C.POINTER(C.c_size_t)]
+        L.swe_ipc_open.argtypes = [vp, C.c_void_p]
         L.swe_last_error.argtypes = [vp]
         L.swe_last_error.restype = C.c_char_p
         L.swe_profile.argtypes = [vp, C.c_int]
@@ -156,6 +161,7 @@ def _params(p: dict | None, device=0, stream=None, alloc=None, part=None) -> Swe
     sp.use_tvb = int(p.get("use_tvb", 1))
     sp.precision = int(p.get("precision", 64))  # 32: FP32 variant
     sp.mrab_coupling = int(p.get("mrab_coupling", 0))  # 1: Alg. 1 printed order, latest committed (NEXT-4)
+    sp.record_decisions = int(p.get("record_decisions", 0))  # decision log for oracle replay
     sp.device = int(device)
     sp.stream = stream
     if alloc is not None:
@@ -315,10 +321,23 @@ class Solver:
     def step(self, dt, nlevels=1):
         _check(lib().swe_step(self._h, float(dt), int(nlevels)), self._h)
 
+    def set_boundary_state(self, h, hu, hv):
+        """Dirichlet boundary data (include/swe.h, reading A7''): nodal state [K, Np] x 3."""
+        h, hu, hv = self._shape(h), self._shape(hu), self._shape(hv)
+        _check(lib().swe_set_boundary_state(self._h, _p(h), _p(hu), _p(hv)), self._h)
+
+    def _out(self, a):
+        """An output buffer the library may write K*Np doubles into: float64, C-contiguous, K*Np elements."""
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous or \
+                a.size != self.K * self.Np or not a.flags.writeable:
+            raise ValueError(f"output buffer must be a writeable C-contiguous float64 array of {self.K * self.Np} "
+                             f"elements")
+        return a
+
     def get_state(self, out=None):
         if out is None:
             out = tuple(np.zeros((self.K, self.Np)) for _ in range(3))
-        h, hu, hv = out
+        h, hu, hv = (self._out(a) for a in out)
         _check(lib().swe_get_state(self._h, _p(h), _p(hu), _p(hv)), self._h)
         return h, hu, hv
 
@@ -328,6 +347,7 @@ class Solver:
 
     def get_state_into(self, h, hu, hv):
         """Write into caller-provided (e.g. pinned) contiguous float64 buffers of K*Np elements."""
+        h, hu, hv = self._out(h), self._out(hu), self._out(hv)
         _check(lib().swe_get_state(self._h, _p(h), _p(hu), _p(hv)), self._h)
 
     def levels(self):
@@ -346,6 +366,29 @@ class Solver:
         _check(lib().swe_get_info(self._h, C.byref(inf)), self._h)
         return {k: (list(getattr(inf, k)) if k == "level_count" else getattr(inf, k)) for k, _ in SweInfo._fields_}
 
+    def ipc_handle(self) -> bytes:
+        """This rank's CUDA-IPC exchange-block handle (include/swe.h, swe_ipc_handle)."""
+        n = C.c_size_t(0)
+        _check(lib().swe_ipc_handle(self._h, None, C.byref(n)), self._h)
+        buf = C.create_string_buffer(n.value)
+        _check(lib().swe_ipc_handle(self._h, buf, C.byref(n)), self._h)
+        return buf.raw[:n.value]
+
+    def ipc_open(self, blobs):
+        """Map every rank's exchange block (blobs in rank order) and use the CUDA-IPC transport."""
+        raw = b"".join(bytes(b) for b in blobs)
+        self._ipc_blobs = C.create_string_buffer(raw, len(raw))
+        _check(lib().swe_ipc_open(self._h, self._ipc_blobs), self._h)
+
+    def decisions(self):
+        """Limiter decision log (params record_decisions=1): uint8 [nrec, K] (include/swe.h)."""
+        n = C.c_int64(0)
+        _check(lib().swe_get_decisions(self._h, None, C.byref(n)), self._h)
+        out = np.zeros((n.value, self.K), dtype=np.uint8)
+        if n.value:
+            _check(lib().swe_get_decisions(self._h, out.ctypes.data_as(C.c_void_p), C.byref(n)), self._h)
+        return out
+
     def profile(self, on: bool):
         _check(lib().swe_profile(self._h, int(on)), self._h)
 
@@ -356,6 +399,14 @@ class Solver:
         _check(lib().swe_profile_read(self._h, _p(t), _p(n, C.c_int64), _p(b)), self._h)
         return {"k1_ms": t[0], "k2_ms": t[1], "k1_launches": int(n[0]), "k2_launches": int(n[1]),
                 "k1_bytes": b[0], "k2_bytes": b[1]}
+
+
+def ipc_connect(solver, group=None):
+    """Exchange the CUDA-IPC handles of all ranks over torch.distributed (plumbing only) and open them."""
+    import torch.distributed as dist
+    blobs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(blobs, solver.ipc_handle(), group=group)
+    solver.ipc_open(blobs)
 
 
 def link_group(solvers):

@@ -8,7 +8,7 @@
 
 namespace swe {
 
-constexpr int kMaxOrder = 4;  // device operators live in constant memory
+constexpr int kMaxOrder = 5;  // device kernels are instantiated for N = 1..5
 
 // Row-major dense matrix.
 struct DMat {
@@ -45,7 +45,7 @@ struct HostMesh {
   std::vector<int32_t> etoe;   // K*3
   std::vector<int8_t> etof;    // K*3
   std::vector<double> hk;      // incircle diameter
-  std::vector<int8_t> bc;      // K*3: boundary faces 0 reflective wall, 1 transmissive outflow (A7')
+  std::vector<int8_t> bc;      // K*3: boundary faces 0 reflective wall, 1 transmissive outflow (A7'), 2 Dirichlet (A7'')
 };
 // Outflow tags from vertex tags (swe_mesh.vbc, NULL = all walls).
 void apply_boundary_tags(HostMesh &m, const int8_t *vbc);

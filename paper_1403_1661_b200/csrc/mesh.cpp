@@ -343,7 +343,8 @@ void apply_boundary_tags(HostMesh &m, const int8_t *vbc) {
       const size_t i = (size_t)3 * e + f;
       if (m.etoe[i] != e || m.etof[i] != f) continue;  // interior face
       const int a = m.etov[(size_t)3 * e + f], b = m.etov[(size_t)3 * e + (f + 1) % 3];
-      m.bc[i] = (vbc[a] == 1 && vbc[b] == 1) ? 1 : 0;
+      // both vertices tagged: the face takes the smaller tag (1 outflow, 2 Dirichlet); otherwise a wall
+      m.bc[i] = (vbc[a] >= 1 && vbc[b] >= 1) ? (int8_t)std::min(std::min((int)vbc[a], (int)vbc[b]), 2) : 0;
     }
 }
 

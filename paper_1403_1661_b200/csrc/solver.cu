@@ -1,8 +1,10 @@
 // solver.cu -- context, MRAB scheduler and C ABI (include/swe.h) of the
 // B200-native DG shallow-water solver.  Device work: kernels.cuh (hot path)
 // plus the setup / permutation / diagnostics kernels below.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -16,6 +18,14 @@
 #include "kernels.cuh"
 
 namespace swe {
+
+// NVTX ranges (header-only NVTX3: no-ops unless a profiler injects itself) around the host driver's phases
+struct Nvtx {
+  explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+static const char *kLevelRange[9] = {"update L0", "update L1", "update L2", "update L3", "update L4",
+                                     "update L5", "update L6", "update L7", "update L8"};
 
 // ------------------------------------------------------------------ setup kernels
 // a_e of every element from the staged caller-layout state, with IEEE
@@ -82,6 +92,18 @@ __global__ void k_scatter_state(int K, int Np, const int *orig, const double *h,
     Q[eb_at(k, i, 3 * Np)] = (T)h[e * Np + i];
     Q[eb_at(k, Np + i, 3 * Np)] = (T)hu[e * Np + i];
     Q[eb_at(k, 2 * Np + i, 3 * Np)] = (T)hv[e * Np + i];
+  }
+}
+
+// cell means of a T-typed element-blocked nodal state ([K/32][3 Np][32]) -> [K/32][3][32], wm2 = mean weights
+template <typename T>
+__global__ void k_cell_means(int K, int Np, const T *Q, const double *wm2, T *means) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= K) return;
+  for (int f = 0; f < 3; f++) {
+    double m = 0.0;
+    for (int i = 0; i < Np; i++) m = fma(wm2[i], (double)Q[eb_at(e, f * Np + i, 3 * Np)], m);
+    means[eb_at(e, f, 3)] = (T)m;
   }
 }
 
@@ -211,13 +233,18 @@ __global__ void k_diag(const __grid_constant__ GatherParams p, const double *V, 
 // ------------------------------------------------------------------ context
 struct Ctx;
 
-// One exchange table per level: entries [level][peer] (send: owned boundary
-// elements, recv: ghosts), each peer's list in global-id order.
+// Exchange table of one phase (A: elements, B: element faces) and one direction.  Entries of a level
+// are contiguous in the index arrays ([level][peer] order, each peer's list in the order both ranks
+// agree on); the BUFFER layout is [level][peer] for receives and [peer][level] for sends, so that the
+// sender's segment for (level l, receiver) starts at base[peer] + (the receiver's own counts of the
+// levels below l) -- what a receiver needs to read a peer's send buffer directly (CUDA-IPC transport).
 struct XTable {
-  std::vector<int> cnt;  // [(L+1) * npeer]  (level 1..L)
-  std::vector<int> off;  // start of (level, peer) within the flattened index array
-  std::vector<int> loff; // start of level l block: loff[l-1] .. loff[l]
+  std::vector<int> cnt;   // [(L+1) * npeer]  (level 1..L)
+  std::vector<int> off;   // buffer position (entries) of segment (level, peer)
+  std::vector<int> loff;  // index-array range of level l: [loff[l-1], loff[l])
+  std::vector<int> base;  // sends: first buffer position of peer i's block ([peer][level] layout)
   int total = 0;
+  int didx = 0, ddst = -1;  // offsets of this table's entry and destination arrays in the device block
 };
 
 struct Ctx {
@@ -245,14 +272,24 @@ struct Ctx {
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
   double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
   double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dOpsGf = nullptr, *dRmin = nullptr;
+  double *dGather = nullptr;             // caller-layout state for swe_get_state (allocated on first use)
+  double *dBndStage = nullptr;           // Dirichlet boundary state, caller layout [3][Kin][Np] (A7'')
+  double *dQbnd = nullptr, *dBmean = nullptr;  // ... in the internal layout, and its cell means
+  bool bnd_set = false;
+  long n_dirichlet = 0;                  // Dirichlet faces of the given mesh (counted at swe_create)
   double *dHk = nullptr;                 // host Hk (caller order), for the device binning
   int32_t *dLev = nullptr, *dLevRes = nullptr;  // binned levels; levels of the resident layout
   int *dFlag = nullptr;
   bool levres_ok = false;  // dLevRes holds the levels of the resident layout
   double *dXsBuf = nullptr, *dXrBuf = nullptr;
-  int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXsIdx = nullptr, *dXrIdx = nullptr;
-  size_t xcap = 0;  // capacity (entries) of the exchange index/buffer arrays
+  int *dE2E = nullptr, *dTcode = nullptr, *dOrig = nullptr, *dXidx = nullptr;
+  size_t capS = 0, capR = 0;  // exchange buffer capacities (T values): max over the two phases' payloads
+  // phase entry lists per peer (given-mesh codes: A element, B (element << 2) | face), in the agreed order
+  std::vector<std::vector<int64_t>> sendA, recvA, sendB, recvB;
   unsigned char *dDry = nullptr;
+  unsigned char *dDec = nullptr;            // decision log of the update in flight (record_decisions, A26)
+  std::vector<unsigned char> declog;        // host log: ndec records of Kin bytes (caller order)
+  long ndec = 0;
   unsigned long long *dCounters = nullptr;
   unsigned long long *hCounters = nullptr;  // pinned
   double *hInjected = nullptr;              // pinned
@@ -265,7 +302,20 @@ struct Ctx {
   std::vector<int32_t> level;  // given-mesh order
   std::vector<int32_t> order;  // internal k -> given-mesh e (owned first, then ghosts)
   int off[9] = {0}, goff[9] = {0};
-  XTable xs, xr;
+  XTable xs[2], xr[2];  // [phase]: 0 = A (means, dry flags; element entries), 1 = B (face traces)
+  int bnd[9] = {0};      // owned level l: boundary elements [off[l-1], bnd[l]), interior [bnd[l], off[l])
+  long xcount = 0;       // exchanges done (identical on every rank: the schedule is global)
+  // CUDA-IPC transport (SURVEY 8(e) NVLink peer memory): every rank's exchange block is mapped by every
+  // other rank; a receiver copies its segments straight out of the sender's send slot
+  bool ipc = false;
+  char *ipcBlock = nullptr;     // own block: header (flags, r_min words), send slots 0 and 1
+  size_t ipcSlotBytes = 0;
+  std::vector<char *> ipcPeer;  // [nranks]: mapped blocks of the other ranks (nullptr for self)
+  std::vector<size_t> ipcPeerSlot;  // [nranks]: their send-slot sizes (ranks' send volumes differ)
+  std::vector<long> ipcBaseA, ipcBaseB;  // [peer index]: the peer's send-layout base of its block for me
+  long rcount = 0;              // r_min reductions done (IPC)
+  cudaStream_t cstream = nullptr;          // communication stream (multi-rank overlap)
+  cudaEvent_t xev[4] = {nullptr, nullptr, nullptr, nullptr};
   int kcount[9] = {0}, par[9] = {0};
   long tick_s[9] = {0}, t_e[9] = {0};
   long tick = 0;
@@ -285,6 +335,7 @@ struct Ctx {
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;      // (start, stop) pairs recorded this macro step
+  std::vector<int> evwhich;         // kernel (0 K1, 1 K2) of each pair
   std::vector<cudaEvent_t> evpool;  // created once, reused
   size_t evnext = 0;
   double prof_ms[2] = {0, 0}, prof_bytes[2] = {0, 0};
@@ -338,20 +389,7 @@ static int cuda_fail(Ctx *c, cudaError_t e, const char *where) {
 
 template <int N, typename T>
 static void fill_ops(const RefOps &o, Ops<N, T> &h) {
-  constexpr int Np = Ops<N>::Np, Nc = Ops<N>::Nc, Ng = Ops<N>::Ng, Nfp = Ops<N>::Nfp;
-  for (int c = 0; c < Nc; c++)
-    for (int i = 0; i < Np; i++) {
-      h.Ic[c][i] = (T)o.Ic(c, i);
-      h.IcDr[c][i] = (T)o.IcDr(c, i);
-      h.IcDs[c][i] = (T)o.IcDs(c, i);
-      h.Pr[i][c] = (T)o.Pr(i, c);
-      h.Ps[i][c] = (T)o.Ps(i, c);
-      h.P[i][c] = (T)o.P(i, c);
-    }
-  for (int i = 0; i < Np; i++)
-    for (int g = 0; g < 3 * Ng; g++) h.Lg[i][g] = (T)o.Lg(i, g);
-  for (int j = 0; j < Ng; j++)
-    for (int k = 0; k < Nfp; k++) h.Ig1[j][k] = (T)o.Ig1(j, k);
+  constexpr int Np = Ops<N>::Np;
   for (int i = 0; i < Np; i++) {
     h.wm2[i] = (T)(0.5 * o.wmean[i]);
     for (int v = 0; v < 3; v++) h.Pv[v][i] = (T)o.Pv(v, i);
@@ -368,10 +406,9 @@ static cudaError_t upload_ops(const RefOps &o) {
   Ops<N, float> hf;
   fill_ops<N, double>(o, h);
   fill_ops<N, float>(o, hf);
-  const void *sym = N == 1 ? (const void *)&c_ops1
-                           : (N == 2 ? (const void *)&c_ops2 : (N == 3 ? (const void *)&c_ops3 : (const void *)&c_ops4));
-  const void *symf = N == 1 ? (const void *)&c_opsf1
-                            : (N == 2 ? (const void *)&c_opsf2 : (N == 3 ? (const void *)&c_opsf3 : (const void *)&c_opsf4));
+  const void *syms[5] = {&c_ops1, &c_ops2, &c_ops3, &c_ops4, &c_ops5};
+  const void *symfs[5] = {&c_opsf1, &c_opsf2, &c_opsf3, &c_opsf4, &c_opsf5};
+  const void *sym = syms[N - 1], *symf = symfs[N - 1];
   cudaError_t e = cudaMemcpyToSymbol(sym, &h, sizeof(h));
   if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(symf, &hf, sizeof(hf));
@@ -423,6 +460,7 @@ static std::vector<double> smem_ops_any(const RefOps &o) {
     case 2: return smem_ops<2>(o);
     case 3: return smem_ops<3>(o);
     case 4: return smem_ops<4>(o);
+    case 5: return smem_ops<5>(o);
   }
   return {};
 }
@@ -433,6 +471,7 @@ static cudaError_t upload_ops_any(const RefOps &o) {
     case 2: return upload_ops<2>(o);
     case 3: return upload_ops<3>(o);
     case 4: return upload_ops<4>(o);
+    case 5: return upload_ops<5>(o);
   }
   return cudaErrorInvalidValue;
 }
@@ -441,7 +480,8 @@ template <int N, bool INIT, typename T>
 static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
-  size_t smem = INIT ? 0 : (size_t)k1_ops_bytes<N, T>();
+  size_t smem = INIT ? 0 : (size_t)k1_ops_bytes<N, T>() + k1_nbr_bytes<N, T>();
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_rhs_update<N, INIT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = (n + K1_BLOCK - 1) / K1_BLOCK;
 #if K1_PERSIST
   int resident = 0;  // SMs x resident blocks per SM (per launch: devices differ)
@@ -488,6 +528,7 @@ static void launch_t(int which, bool init, int N, const StepParamsT<T> &p, cudaS
       case 2: init ? launch_k1<2, true, T>(p, s) : launch_k1<2, false, T>(p, s); break;
       case 3: init ? launch_k1<3, true, T>(p, s) : launch_k1<3, false, T>(p, s); break;
       case 4: init ? launch_k1<4, true, T>(p, s) : launch_k1<4, false, T>(p, s); break;
+      case 5: init ? launch_k1<5, true, T>(p, s) : launch_k1<5, false, T>(p, s); break;
     }
   } else {
     switch (N) {
@@ -495,6 +536,7 @@ static void launch_t(int which, bool init, int N, const StepParamsT<T> &p, cudaS
       case 2: launch_k2<2, T>(p, s); break;
       case 3: launch_k2<3, T>(p, s); break;
       case 4: launch_k2<4, T>(p, s); break;
+      case 5: launch_k2<5, T>(p, s); break;
     }
   }
 }
@@ -519,7 +561,8 @@ static StepParamsT<float> to_f32(const StepParams &d) {
   f.g = (float)d.g, f.h0 = (float)d.h0, f.eps = (float)d.eps, f.e4 = (float)d.e4;
   f.tvb_M = (float)d.tvb_M, f.tvb_nu = (float)d.tvb_nu, f.h_char = (float)d.h_char;
   f.use_pp = d.use_pp, f.use_tvb = d.use_tvb;
-  f.counters = d.counters, f.injected = d.injected, f.opsG = (const float *)d.opsG;
+  f.counters = d.counters, f.injected = d.injected, f.opsG = (const float *)d.opsG, f.dec = d.dec;
+  f.Qbnd = (const float *)d.Qbnd, f.bmean = (const float *)d.bmean;
   return f;
 }
 
@@ -568,6 +611,9 @@ static StepParams base_params(Ctx *c) {
   p.use_tvb = c->prm.use_tvb;
   p.counters = c->dCounters;
   p.injected = c->dInjected;
+  p.dec = c->dDec;
+  p.Qbnd = c->dQbnd;
+  p.bmean = c->dBmean;
   p.opsG = c->f32 ? c->dOpsGf : c->dOpsG;
   p.nlev = c->L;
   p.kown = c->kown;
@@ -578,6 +624,7 @@ static StepParams base_params(Ctx *c) {
   return p;
 }
 
+static void build_entry_lists(Ctx *c);
 static int alloc_state(Ctx *c) {
   if (c->dQ) return SWE_OK;
   size_t K = c->K, Np = c->Np, Kin = c->Kin;
@@ -597,17 +644,22 @@ static int alloc_state(Ctx *c) {
   c->dE2E = (int *)c->dalloc(sizeof(int) * 3 * Kp);
   c->dTcode = (int *)c->dalloc(sizeof(int) * K);
   c->dOrig = (int *)c->dalloc(sizeof(int) * K);
-  c->dDry = (unsigned char *)c->dalloc(K);
+  c->dDry = (unsigned char *)c->dalloc((size_t)4 * K);  // [K][4] dry words (kernels.cuh store_dry)
+  if (c->prm.record_decisions) c->dDec = (unsigned char *)c->dalloc(K);
   c->dPartials = (double *)c->dalloc(sizeof(double) * 2 * ((K + 255) / 256));
   c->dRmin = (double *)c->dalloc(sizeof(double));
-  size_t ns = 0, nr = 0;
-  for (auto &v : c->plan.send) ns += v.size();
-  for (auto &v : c->plan.recv) nr += v.size();
-  c->xcap = std::max(ns, nr) + 1;
-  c->dXsIdx = (int *)c->dalloc(sizeof(int) * c->xcap);
-  c->dXrIdx = (int *)c->dalloc(sizeof(int) * c->xcap);
-  c->dXsBuf = (double *)c->dalloc(es * 6 * Np * c->xcap);
-  c->dXrBuf = (double *)c->dalloc(es * 6 * Np * c->xcap);
+  // exchange entry lists (level-independent) and buffer capacities
+  build_entry_lists(c);
+  size_t nsA = 0, nrA = 0, nsB = 0, nrB = 0;
+  for (auto &v : c->sendA) nsA += v.size();
+  for (auto &v : c->recvA) nrA += v.size();
+  for (auto &v : c->sendB) nsB += v.size();
+  for (auto &v : c->recvB) nrB += v.size();
+  const size_t Nfp = (size_t)c->N + 1;
+  c->capS = std::max((size_t)4 * nsA, 6 * Nfp * nsB) + 8;
+  c->capR = std::max((size_t)4 * nrA, 6 * Nfp * nrB) + 8;
+  c->dXsBuf = (double *)c->dalloc(es * c->capS);
+  c->dXrBuf = (double *)c->dalloc(es * c->capR);
   if (!c->alloc_ok) {
     c->err = "device allocation failed";
     return SWE_ERR_NOMEM;
@@ -615,106 +667,231 @@ static int alloc_state(Ctx *c) {
   return SWE_OK;
 }
 
-// Exchange tables for the current internal order: entries [level][peer].
-static void build_xtable(Ctx *c, const std::vector<std::vector<int32_t>> &lists, const std::vector<int32_t> &inv,
-                         XTable &t, std::vector<int> &flat) {
-  const int np = (int)c->plan.peers.size(), L = c->L;
-  t.cnt.assign((size_t)(L + 1) * std::max(np, 1), 0);
-  t.off.assign((size_t)(L + 1) * std::max(np, 1), 0);
+// ------------------------------------------------------------------ halo exchange tables
+// Entry lists of both phases, per peer, in the order both ranks derive independently:
+//   phase A: the halo plan's element lists (global-id order);
+//   phase B: the faces of those elements that border the other rank -- sends: faces of my boundary
+//            elements whose neighbour the peer owns; receives: faces of the peer's ghosts whose neighbour
+//            I own -- per element ordered by the global id of the element across the face.
+static void face_entries(const Ctx *c, const std::vector<int32_t> &elems, int other, std::vector<int64_t> &out) {
+  out.clear();
+  for (int e : elems) {
+    int fs[3], n = 0;
+    for (int f = 0; f < 3; f++) {
+      const int nb = c->mesh.etoe[(size_t)3 * e + f];
+      if (nb != e && c->owner[nb] == other) fs[n++] = f;
+    }
+    std::sort(fs, fs + n, [&](int a, int b) {
+      const int64_t ga = c->gid[c->mesh.etoe[(size_t)3 * e + a]], gb = c->gid[c->mesh.etoe[(size_t)3 * e + b]];
+      return ga != gb ? ga < gb : a < b;
+    });
+    for (int j = 0; j < n; j++) out.push_back(((int64_t)e << 2) | fs[j]);
+  }
+}
+static void build_entry_lists(Ctx *c) {
+  const size_t np = c->plan.peers.size();
+  c->sendA.assign(np, {});
+  c->recvA.assign(np, {});
+  c->sendB.assign(np, {});
+  c->recvB.assign(np, {});
+  for (size_t i = 0; i < np; i++) {
+    c->sendA[i].assign(c->plan.send[i].begin(), c->plan.send[i].end());
+    c->recvA[i].assign(c->plan.recv[i].begin(), c->plan.recv[i].end());
+    face_entries(c, c->plan.send[i], c->plan.peers[i], c->sendB[i]);
+    face_entries(c, c->plan.recv[i], c->rank, c->recvB[i]);
+  }
+}
+
+// Table of one phase and direction for the current internal order (inv: given -> internal index).
+// Appends the entry array (internal codes, [level][peer] order) and, for sends, the destination array to
+// `blk`, recording their offsets in t.didx / t.ddst.
+static void build_xtable(Ctx *c, const std::vector<std::vector<int64_t>> &lists, bool faces, bool send,
+                         const std::vector<int32_t> &inv, XTable &t, std::vector<int> &blk) {
+  const int np = (int)lists.size(), L = c->L, NP = std::max(np, 1);
+  auto elem = [&](int64_t code) { return (int)(faces ? code >> 2 : code); };
+  t.cnt.assign((size_t)(L + 1) * NP, 0);
+  t.off.assign((size_t)(L + 1) * NP, 0);
   t.loff.assign(L + 2, 0);
-  flat.clear();
-  for (int l = 1; l <= L; l++) {
-    t.loff[l - 1] = (int)flat.size();
+  t.base.assign(np + 1, 0);
+  for (int i = 0; i < np; i++)
+    for (int64_t code : lists[i]) t.cnt[(size_t)c->level[elem(code)] * NP + i]++;
+  for (int i = 0; i < np; i++) t.base[i + 1] = t.base[i] + (int)lists[i].size();
+  if (send) {
     for (int i = 0; i < np; i++) {
-      t.off[(size_t)l * np + i] = (int)flat.size();
-      for (int e : lists[i])
-        if (c->level[e] == l) flat.push_back(inv[e]);
-      t.cnt[(size_t)l * np + i] = (int)flat.size() - t.off[(size_t)l * np + i];
+      int o = t.base[i];
+      for (int l = 1; l <= L; l++) {
+        t.off[(size_t)l * NP + i] = o;
+        o += t.cnt[(size_t)l * NP + i];
+      }
+    }
+  } else {
+    int o = 0;
+    for (int l = 1; l <= L; l++)
+      for (int i = 0; i < np; i++) {
+        t.off[(size_t)l * NP + i] = o;
+        o += t.cnt[(size_t)l * NP + i];
+      }
+  }
+  std::vector<int> idx, dst;
+  for (int l = 1; l <= L; l++) {
+    t.loff[l - 1] = (int)idx.size();
+    for (int i = 0; i < np; i++) {
+      int j = 0;
+      for (int64_t code : lists[i]) {
+        const int e = elem(code);
+        if (c->level[e] != l) continue;
+        idx.push_back(faces ? (inv[e] << 2) | (int)(code & 3) : inv[e]);
+        dst.push_back(t.off[(size_t)l * NP + i] + j++);
+      }
     }
   }
-  t.loff[L] = (int)flat.size();
-  t.total = (int)flat.size();
+  t.loff[L] = (int)idx.size();
+  t.total = (int)idx.size();
+  t.didx = (int)blk.size();
+  blk.insert(blk.end(), idx.begin(), idx.end());
+  t.ddst = -1;
+  if (send) {
+    t.ddst = (int)blk.size();
+    blk.insert(blk.end(), dst.begin(), dst.end());
+  }
 }
 
 // ------------------------------------------------------------------ halo exchange (pack / transfer / unpack)
-static int payload(Ctx *c, int phase) { return phase == 0 ? 4 : 6 * c->Np; }
+static int payload(Ctx *c, int phase) { return phase == 0 ? 4 : 6 * (c->N + 1); }
+constexpr size_t kIpcHdr = 256;  // IPC block header: u64 flag[2] @0, u64 rflag[2] @16, double rmin[2] @32
+
+// send buffer of exchange k: the IPC block's slot (k mod 2) -- a peer may still be reading slot k-1 -- or
+// the plain device buffer (NCCL, in-process)
+static char *send_buf(Ctx *c, long k) {
+  if (c->ipc) return c->ipcBlock + kIpcHdr + (size_t)(k & 1) * c->ipcSlotBytes;
+  return (char *)c->dXsBuf;
+}
+
+static void halo_launch(Ctx *c, bool pack, int phase, int a, int b, int par, int slot, cudaStream_t s, char *buf,
+                        const XTable &t) {
+  auto run = [&](auto tag) {
+    using T = decltype(tag);
+    HaloParamsT<T> h;
+    std::memset(&h, 0, sizeof(h));
+    h.n = b - a;
+    h.K = c->K;
+    h.N = c->N;
+    h.Np = c->Np;
+    h.Nfp = c->N + 1;
+    h.phase = phase;
+    h.par = par;
+    h.slot = slot;
+    h.idx = c->dXidx + t.didx + a;
+    h.dst = pack ? c->dXidx + t.ddst + a : nullptr;
+    h.buf = pack ? (T *)buf : (T *)buf + (size_t)payload(c, phase) * a;
+    h.Q = (T *)c->dQ;
+    h.R = (T *)c->dR;
+    h.means = (T *)c->dMeans;
+    h.dry = c->dDry;
+    h.kown = c->kown;
+    h.E2E = c->dE2E;
+    if (pack)
+      k_halo_pack<T><<<(h.n + 127) / 128, 128, 0, s>>>(h);
+    else
+      k_halo_unpack<T><<<(h.n + 127) / 128, 128, 0, s>>>(h);
+  };
+  if (c->f32)
+    run(float{});
+  else
+    run(double{});
+}
 
 // lvl = 0: all levels (initial exchange), else one level
-static int xpack(Ctx *c, int phase, int lvl, int par, int slot) {
+static int xpack(Ctx *c, int phase, int lvl, int par, int slot, cudaStream_t s, long k) {
   if (c->plan.peers.empty()) return SWE_OK;
-  int a = lvl == 0 ? 0 : c->xs.loff[lvl - 1], b = lvl == 0 ? c->xs.total : c->xs.loff[lvl];
+  const XTable &t = c->xs[phase];
+  int a = lvl == 0 ? 0 : t.loff[lvl - 1], b = lvl == 0 ? t.total : t.loff[lvl];
   if (b <= a) return SWE_OK;
-  auto run = [&](auto tag) {
-    using T = decltype(tag);
-    HaloParamsT<T> h;
-    std::memset(&h, 0, sizeof(h));
-    h.n = b - a;
-    h.K = c->K;
-    h.Np = c->Np;
-    h.phase = phase;
-    h.par = par;
-    h.slot = slot;
-    h.idx = c->dXsIdx + a;
-    h.buf = (T *)c->dXsBuf + (size_t)payload(c, phase) * a;
-    h.Q = (T *)c->dQ;
-    h.R = (T *)c->dR;
-    h.means = (T *)c->dMeans;
-    h.dry = c->dDry;
-    k_halo_pack<T><<<(h.n + 127) / 128, 128, 0, c->stream>>>(h);
-  };
-  if (c->f32)
-    run(float{});
-  else
-    run(double{});
+  halo_launch(c, true, phase, a, b, par, slot, s, send_buf(c, k), t);
   CK(cudaGetLastError());
   return SWE_OK;
 }
 
-static int xunpack(Ctx *c, int phase, int lvl, int par, int slot) {
+static int xunpack(Ctx *c, int phase, int lvl, int par, int slot, cudaStream_t s) {
   if (c->plan.peers.empty()) return SWE_OK;
-  int a = lvl == 0 ? 0 : c->xr.loff[lvl - 1], b = lvl == 0 ? c->xr.total : c->xr.loff[lvl];
+  const XTable &t = c->xr[phase];
+  int a = lvl == 0 ? 0 : t.loff[lvl - 1], b = lvl == 0 ? t.total : t.loff[lvl];
   if (b <= a) return SWE_OK;
-  auto run = [&](auto tag) {
-    using T = decltype(tag);
-    HaloParamsT<T> h;
-    std::memset(&h, 0, sizeof(h));
-    h.n = b - a;
-    h.K = c->K;
-    h.Np = c->Np;
-    h.phase = phase;
-    h.par = par;
-    h.slot = slot;
-    h.idx = c->dXrIdx + a;
-    h.buf = (T *)c->dXrBuf + (size_t)payload(c, phase) * a;
-    h.Q = (T *)c->dQ;
-    h.R = (T *)c->dR;
-    h.means = (T *)c->dMeans;
-    h.dry = c->dDry;
-    k_halo_unpack<T><<<(h.n + 127) / 128, 128, 0, c->stream>>>(h);
-  };
-  if (c->f32)
-    run(float{});
-  else
-    run(double{});
+  halo_launch(c, false, phase, a, b, par, slot, s, (char *)c->dXrBuf, t);
   CK(cudaGetLastError());
   return SWE_OK;
 }
 
-// transfer: NCCL point-to-point (one group per exchange) or in-process peers
-static int xtransfer(Ctx *c, int phase, int lvl) {
+// ---- stream memory operations (driver API, resolved at run time: the library does not link libcuda)
+typedef CUresult (*PfnWait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PfnWrite64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+static PfnWait64 g_wait64 = nullptr;
+static PfnWrite64 g_write64 = nullptr;
+static unsigned g_wait_flush = 0;
+static int memops_init(Ctx *c) {
+  if (g_wait64 && g_write64) return SWE_OK;
+  cudaDriverEntryPointQueryResult q1, q2;
+  void *f1 = nullptr, *f2 = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f1, cudaEnableDefault, &q1) != cudaSuccess || !f1 ||
+      cudaGetDriverEntryPoint("cuStreamWriteValue64", &f2, cudaEnableDefault, &q2) != cudaSuccess || !f2) {
+    c->err = "stream memory operations (cuStreamWaitValue64) unavailable";
+    return SWE_ERR_CUDA;
+  }
+  int flush = 0;
+  cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, c->device);
+  g_wait_flush = flush ? (unsigned)CU_STREAM_WAIT_VALUE_FLUSH : 0u;
+  g_wait64 = (PfnWait64)f1;
+  g_write64 = (PfnWrite64)f2;
+  return SWE_OK;
+}
+// flag value of exchange k in the parity word k mod 2.  A rank writes value(k+2) into that word only after
+// it has waited for every peer's value(k+1), which each peer writes after its own wait on value(k) has
+// passed: an equality wait can therefore never miss its value.
+static cuuint64_t flag_value(long k) { return (cuuint64_t)(k % (1L << 40)) + 1; }
+
+// transfer of exchange k (NCCL point-to-point, in-process peers, or CUDA IPC), enqueued on stream s
+static int xtransfer(Ctx *c, int phase, int lvl, cudaStream_t s, long k) {
   const int np = (int)c->plan.peers.size();
   if (np == 0) return SWE_OK;
   const int P = payload(c, phase);
+  const XTable &xs = c->xs[phase], &xr = c->xr[phase];
+  const int l0 = lvl == 0 ? 1 : lvl, l1 = lvl == 0 ? c->L : lvl;
+  if (c->ipc) {
+    const int sl = (int)(k & 1);
+    const cuuint64_t v = flag_value(k);
+    if (g_write64((CUstream)s, (CUdeviceptr)(c->ipcBlock + 8 * sl), v, 0) != CUDA_SUCCESS) {
+      c->err = "cuStreamWriteValue64 failed";
+      return SWE_ERR_CUDA;
+    }
+    for (int i = 0; i < np; i++) {
+      char *pb = c->ipcPeer[c->plan.peers[i]];
+      if (g_wait64((CUstream)s, (CUdeviceptr)(pb + 8 * sl), v, CU_STREAM_WAIT_VALUE_EQ | g_wait_flush) !=
+          CUDA_SUCCESS) {
+        c->err = "cuStreamWaitValue64 failed";
+        return SWE_ERR_CUDA;
+      }
+      const char *src = pb + kIpcHdr + (size_t)sl * c->ipcPeerSlot[c->plan.peers[i]];
+      long so = phase == 0 ? c->ipcBaseA[i] : c->ipcBaseB[i];
+      for (int l = 1; l <= c->L; l++) {
+        const int rc = xr.cnt[(size_t)l * np + i];
+        if (l >= l0 && l <= l1 && rc > 0)
+          CK(cudaMemcpyAsync((char *)c->dXrBuf + c->esz * P * xr.off[(size_t)l * np + i], src + c->esz * P * so,
+                             c->esz * P * rc, cudaMemcpyDeviceToDevice, s));
+        so += rc;
+      }
+    }
+    return SWE_OK;
+  }
   if (c->comm) {
     NK(ncclGroupStart());
     for (int i = 0; i < np; i++) {
-      for (int l = (lvl == 0 ? 1 : lvl); l <= (lvl == 0 ? c->L : lvl); l++) {
-        int so = c->xs.off[(size_t)l * np + i], sc = c->xs.cnt[(size_t)l * np + i];
-        int ro = c->xr.off[(size_t)l * np + i], rc = c->xr.cnt[(size_t)l * np + i];
+      for (int l = l0; l <= l1; l++) {
+        int so = xs.off[(size_t)l * np + i], sc = xs.cnt[(size_t)l * np + i];
+        int ro = xr.off[(size_t)l * np + i], rc = xr.cnt[(size_t)l * np + i];
         const ncclDataType_t dt = c->f32 ? ncclFloat : ncclDouble;
         char *sb = (char *)c->dXsBuf, *rb = (char *)c->dXrBuf;
-        if (sc > 0) NK(ncclSend(sb + c->esz * P * so, (size_t)P * sc, dt, c->plan.peers[i], c->comm, c->stream));
-        if (rc > 0) NK(ncclRecv(rb + c->esz * P * ro, (size_t)P * rc, dt, c->plan.peers[i], c->comm, c->stream));
+        if (sc > 0) NK(ncclSend(sb + c->esz * P * so, (size_t)P * sc, dt, c->plan.peers[i], c->comm, s));
+        if (rc > 0) NK(ncclRecv(rb + c->esz * P * ro, (size_t)P * rc, dt, c->plan.peers[i], c->comm, s));
       }
     }
     NK(ncclGroupEnd());
@@ -723,6 +900,10 @@ static int xtransfer(Ctx *c, int phase, int lvl) {
   if (!c->group.empty()) {  // in-process peers on one device: copy out of the peer's send buffer
     for (int i = 0; i < np; i++) {
       Ctx *q = c->group[c->plan.peers[i]];
+      if (!q) {
+        c->err = "in-process group member destroyed";
+        return SWE_ERR_STATE;
+      }
       int qi = -1;
       for (size_t j = 0; j < q->plan.peers.size(); j++)
         if (q->plan.peers[j] == c->rank) qi = (int)j;
@@ -731,21 +912,22 @@ static int xtransfer(Ctx *c, int phase, int lvl) {
         return SWE_ERR_STATE;
       }
       const int qnp = (int)q->plan.peers.size();
-      for (int l = (lvl == 0 ? 1 : lvl); l <= (lvl == 0 ? c->L : lvl); l++) {
-        int ro = c->xr.off[(size_t)l * np + i], rc = c->xr.cnt[(size_t)l * np + i];
-        int so = q->xs.off[(size_t)l * qnp + qi], sc = q->xs.cnt[(size_t)l * qnp + qi];
+      const XTable &qs = q->xs[phase];
+      for (int l = l0; l <= l1; l++) {
+        int ro = xr.off[(size_t)l * np + i], rc = xr.cnt[(size_t)l * np + i];
+        int so = qs.off[(size_t)l * qnp + qi], sc = qs.cnt[(size_t)l * qnp + qi];
         if (rc != sc) {
           c->err = "halo exchange size mismatch";
           return SWE_ERR_STATE;
         }
         if (rc > 0)
           CK(cudaMemcpyAsync((char *)c->dXrBuf + c->esz * P * ro, (char *)q->dXsBuf + c->esz * P * so, c->esz * P * rc,
-                             cudaMemcpyDeviceToDevice, c->stream));
+                             cudaMemcpyDeviceToDevice, s));
       }
     }
     return SWE_OK;
   }
-  c->err = "ranks > 1 without a transport (pass nccl_id or use swe_step_group)";
+  c->err = "ranks > 1 without a transport (swe_ipc_open, nccl_id, or swe_link_group)";
   return SWE_ERR_NCCL;
 }
 
@@ -777,6 +959,16 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   c->L = L;
   std::vector<int32_t> owned_sorted, ghosts_sorted;
   order_subset(c->mesh, levels, c->plan.owned, owned_sorted);
+  // boundary-first within each level (SURVEY 8(e) overlap): elements with a ghost neighbour (the phase-A
+  // send lists) lead their level, so a level update can launch them first and exchange their results
+  // while the interior elements compute.  Single rank: no boundary, order unchanged.
+  std::vector<char> isb(c->Kin, 0);
+  for (auto &lst : c->plan.send)
+    for (int e : lst) isb[e] = 1;
+  std::stable_sort(owned_sorted.begin(), owned_sorted.end(), [&](int a, int b) {
+    if (levels[a] != levels[b]) return levels[a] < levels[b];
+    return isb[a] > isb[b];
+  });
   ghosts_sorted = c->plan.ghosts;
   std::stable_sort(ghosts_sorted.begin(), ghosts_sorted.end(), [&](int a, int b) {
     if (levels[a] != levels[b]) return levels[a] < levels[b];
@@ -811,6 +1003,12 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
       ao += co[l];
       ag += cg[l];
     }
+    for (int l = 1; l <= 8; l++) {
+      int k = c->off[l - 1];
+      const int k1 = l <= L ? c->off[l] : c->kown;
+      while (k < k1 && isb[c->order[k]]) k++;
+      c->bnd[l] = k;
+    }
   }
   // E2E and the TVB alphas are element-blocked ([K/32][rows][32], kernels.cuh), V and TC are [rows][K]
   std::vector<double> V((size_t)6 * K, 0.0), TA((size_t)6 * eb_pad(K), 0.0);
@@ -830,12 +1028,12 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
           c->err = "owned element with a neighbour outside the local set";
           return SWE_ERR_MESH;
         }
-        // boundary faces are self references (n == e, nf == f); a transmissive outflow face (A7')
-        // carries neighbour face code 3 instead
-        const bool outflow = n == e && nf == f && c->mesh.bc[(size_t)3 * e + f] == 1;
-        E2E[eb_at(k, f, 3)] = (inv[n] << 2) | (outflow ? 3 : nf);
-      } else {
-        E2E[eb_at(k, f, 3)] = (k << 2) | f;  // ghosts are never launched
+        // boundary faces are self references (n == e) with face code f for a reflective wall, 3 for a
+        // transmissive outflow face (A7') and (f + 1) mod 3 for a Dirichlet face (A7'')
+        const int tag = (n == e && nf == f) ? c->mesh.bc[(size_t)3 * e + f] : 0;
+        E2E[eb_at(k, f, 3)] = (inv[n] << 2) | (tag == 1 ? 3 : (tag == 2 ? (f + 1) % 3 : nf));
+      } else {  // ghosts are never launched; their rows name their local neighbours (halo unpack A uses them)
+        E2E[eb_at(k, f, 3)] = (n != e && inv[n] >= 0) ? (inv[n] << 2) | nf : (k << 2) | f;
       }
       size_t s = (size_t)3 * e + f;
       code |= (c->tvb.pj[s] & 3) << (4 * f);
@@ -845,9 +1043,18 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
     }
     TC[k] = code;
   }
-  std::vector<int> xsf, xrf;
-  build_xtable(c, c->plan.send, inv, c->xs, xsf);
-  build_xtable(c, c->plan.recv, inv, c->xr, xrf);
+  std::vector<int> xblk;
+  build_xtable(c, c->sendA, false, true, inv, c->xs[0], xblk);
+  build_xtable(c, c->recvA, false, false, inv, c->xr[0], xblk);
+  build_xtable(c, c->sendB, true, true, inv, c->xs[1], xblk);
+  build_xtable(c, c->recvB, true, false, inv, c->xr[1], xblk);
+  c->dfree(c->dXidx);
+  c->dXidx = (int *)c->dalloc(sizeof(int) * std::max<size_t>(xblk.size(), 1));
+  if (!c->dXidx) {
+    c->alloc_ok = true;
+    c->err = "device allocation failed (exchange tables)";
+    return SWE_ERR_NOMEM;
+  }
   CK(cudaMemcpyAsync(c->dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, c->stream));
   std::vector<float> TAf;
   if (c->f32) {
@@ -859,10 +1066,8 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   CK(cudaMemcpyAsync(c->dE2E, E2E.data(), sizeof(int) * E2E.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dTcode, TC.data(), sizeof(int) * TC.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->dOrig, c->order.data(), sizeof(int) * K, cudaMemcpyHostToDevice, c->stream));
-  if (!xsf.empty())
-    CK(cudaMemcpyAsync(c->dXsIdx, xsf.data(), sizeof(int) * xsf.size(), cudaMemcpyHostToDevice, c->stream));
-  if (!xrf.empty())
-    CK(cudaMemcpyAsync(c->dXrIdx, xrf.data(), sizeof(int) * xrf.size(), cudaMemcpyHostToDevice, c->stream));
+  if (!xblk.empty())
+    CK(cudaMemcpyAsync(c->dXidx, xblk.data(), sizeof(int) * xblk.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));  // host vectors above are released on return
   int nb = (K + 127) / 128;
   if (c->f32) {
@@ -879,6 +1084,30 @@ static int materialize(Ctx *c, const std::vector<int32_t> &levels, int L) {
   return materialize_state(c);
 }
 
+// Dirichlet boundary state (A7''): staged caller layout -> internal layout + cell means
+static int scatter_bnd(Ctx *c) {
+  if (!c->bnd_set || !c->layout_valid) return SWE_OK;
+  const int K = c->K, nb = (K + 127) / 128;
+  const size_t KNp = (size_t)c->Kin * c->Np;
+  double *st = c->dBndStage;
+  if (c->f32) {
+    k_scatter_state<float><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, st, st + KNp, st + 2 * KNp, (float *)c->dQbnd);
+    k_cell_means<float><<<nb, 128, 0, c->stream>>>(K, c->Np, (const float *)c->dQbnd, c->dWm2, (float *)c->dBmean);
+  } else {
+    k_scatter_state<double><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, st, st + KNp, st + 2 * KNp, c->dQbnd);
+    k_cell_means<double><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dQbnd, c->dWm2, c->dBmean);
+  }
+  CK(cudaGetLastError());
+  return SWE_OK;
+}
+
+// Dirichlet faces present but no boundary state given
+static int check_bnd(Ctx *c) {
+  if (c->bnd_set || c->n_dirichlet == 0) return SWE_OK;
+  c->err = "the mesh has Dirichlet faces (vbc = 2) but swe_set_boundary_state was not called";
+  return SWE_ERR_STATE;
+}
+
 // State part of materialize: the staged caller-order state into the internal order, fresh
 // dry flags, counters, AB ramp and clocks.
 static int materialize_state(Ctx *c) {
@@ -892,8 +1121,9 @@ static int materialize_state(Ctx *c) {
     k_scatter_state<double><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp,
                                                        c->dStage + 2 * KNp, c->dQ);
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(c->dDry, 0, K, c->stream));
-  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
+  if (int rc = scatter_bnd(c)) return rc;
+  CK(cudaMemsetAsync(c->dDry, 0, (size_t)4 * K, c->stream));
+  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * kCounters * kSlots, c->stream));
   CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream));
   c->n_updates = 0;
   for (int l = 0; l <= 8; l++) {
@@ -1013,6 +1243,7 @@ static void launch_timed(Ctx *c, int which, const StepParams &p) {
     cudaEventRecord(e1, c->stream);
     c->ev.push_back(e0);
     c->ev.push_back(e1);
+    c->evwhich.push_back(which);
     c->prof_bytes[which] += (which == 0 ? k1_bytes(c->N, p.nab, c->prm.use_tvb, c->esz) : k2_bytes(c->esz)) * nel;
     c->prof_launch[which]++;
   } else {
@@ -1021,14 +1252,14 @@ static void launch_timed(Ctx *c, int which, const StepParams &p) {
 }
 
 static void collect_profile(Ctx *c) {
-  // events come in (start, stop) pairs, K1 and K2 interleaved in launch order
+  // events come in (start, stop) pairs, in launch order
   for (size_t i = 0; i + 1 < c->ev.size(); i += 2) {
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
-    int which = (int)((i / 2) % (c->prm.use_tvb ? 2 : 1));
-    c->prof_ms[which] += ms;
+    c->prof_ms[c->evwhich[i / 2]] += ms;
   }
   c->ev.clear();
+  c->evwhich.clear();
   c->evnext = 0;
 }
 
@@ -1102,6 +1333,7 @@ static bool ramp_done(const Ctx *c) {
 }
 
 static int graph_step(Ctx *c) {
+  Nvtx range("macro step: CUDA graph");
   if (!c->gstream) {
     CK(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming));
@@ -1151,33 +1383,107 @@ static int graph_step(Ctx *c) {
   return SWE_OK;
 }
 
-// One MRAB update of level l at tick t for every context of the group, with
-// the two halo exchanges: A (means, dry; after K1) and B (Q, R slot; after K2).
+// Append one decision record (A26) for the owned internal range [k0, k1) of the limiter application just
+// launched (stream-synchronising; record_decisions is a debug mode).
+static int record_dec(Ctx *c, int k0, int k1) {
+  if (!c->dDec) return SWE_OK;
+  std::vector<unsigned char> d((size_t)std::max(0, k1 - k0));
+  if (k1 > k0) CK(cudaMemcpyAsync(d.data(), c->dDec + k0, (size_t)(k1 - k0), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const size_t base = c->declog.size();
+  c->declog.resize(base + (size_t)c->Kin, 0xFF);
+  for (int k = k0; k < k1; k++) c->declog[base + (size_t)c->order[k]] = d[(size_t)(k - k0)];
+  c->ndec++;
+  return SWE_OK;
+}
+
+// One halo exchange of `phase` for every context of the group, on each context's stream: pack into the send
+// buffer of exchange k, transfer, unpack (in-process contexts share one stream, so every pack precedes
+// every transfer).
+static int group_exchange(std::vector<Ctx *> &G, int phase, int lvl, int par, int slot) {
+  Nvtx range(phase == 0 ? "halo A (means, dry)" : "halo B (face traces)");
+  std::vector<long> ks;
+  for (Ctx *c : G) ks.push_back(c->xcount++);
+  for (size_t i = 0; i < G.size(); i++)
+    if (int rc = xpack(G[i], phase, lvl, par, slot, G[i]->stream, ks[i])) return rc;
+  for (size_t i = 0; i < G.size(); i++)
+    if (int rc = xtransfer(G[i], phase, lvl, G[i]->stream, ks[i])) return rc;
+  for (Ctx *c : G)
+    if (int rc = xunpack(c, phase, lvl, par, slot, c->stream)) return rc;
+  return SWE_OK;
+}
+
+// One MRAB update of level l at tick t for every context of an in-process group (one stream), with the
+// two halo exchanges: A (means, dry; after K1) and B (face traces of Q and the R slot; after K2).
 static int group_update(std::vector<Ctx *> &G, int l, long t) {
+  Nvtx range(kLevelRange[l]);
   for (Ctx *c : G) {
     c->cur = update_params(c, l, t);
     launch_timed(c, 0, c->cur);
   }
-  for (Ctx *c : G)
-    if (int rc = xpack(c, 0, l, 0, 0)) return rc;
-  for (Ctx *c : G)
-    if (int rc = xtransfer(c, 0, l)) return rc;
-  for (Ctx *c : G)
-    if (int rc = xunpack(c, 0, l, 0, 0)) return rc;
+  if (int rc = group_exchange(G, 0, l, 0, 0)) return rc;
   for (Ctx *c : G)
     if (c->prm.use_tvb) launch_timed(c, 1, c->cur);
+  if (int rc = group_exchange(G, 1, l, G[0]->cur.write_par, G[0]->cur.write_slot)) return rc;
   for (Ctx *c : G)
-    if (int rc = xpack(c, 1, l, c->cur.write_par, c->cur.write_slot)) return rc;
-  for (Ctx *c : G)
-    if (int rc = xtransfer(c, 1, l)) return rc;
-  for (Ctx *c : G)
-    if (int rc = xunpack(c, 1, l, c->cur.write_par, c->cur.write_slot)) return rc;
+    if (int rc = record_dec(c, c->cur.k0, c->cur.k1)) return rc;
   for (Ctx *c : G) commit_update(c, l, t, c->cur);
+  return SWE_OK;
+}
+
+static int ensure_comm_stream(Ctx *c) {
+  if (c->cstream) return SWE_OK;
+  CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+  for (auto &e : c->xev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return SWE_OK;
+}
+
+// One MRAB update of level l at tick t of a rank of a multi-process partition (CUDA-IPC or NCCL
+// transport), with the exchanges on the communication stream overlapping interior work:
+//   compute: K1(boundary) | pack A |  K1(interior)  | wait A | K2(boundary) | pack B |  K2(interior)  | wait B
+//   comm:                         | exchange A     |                               | exchange B     |
+// Interior elements have no ghost neighbour, so K1(interior) does not read what exchange B of the previous
+// update delivers, and neither interior kernel touches a ghost.
+static int rank_update(Ctx *c, int l, long t) {
+  Nvtx range(kLevelRange[l]);
+  if (int rc = ensure_comm_stream(c)) return rc;
+  const StepParams p = update_params(c, l, t);
+  c->cur = p;
+  StepParams pb = p, pi = p;
+  pb.k1 = c->bnd[l];
+  pi.k0 = c->bnd[l];
+  cudaStream_t S = c->stream, X = c->cstream;
+  launch_timed(c, 0, pb);
+  long k = c->xcount++;
+  if (int rc = xpack(c, 0, l, 0, 0, S, k)) return rc;
+  CK(cudaEventRecord(c->xev[0], S));
+  CK(cudaStreamWaitEvent(X, c->xev[0], 0));
+  if (int rc = xtransfer(c, 0, l, X, k)) return rc;
+  if (int rc = xunpack(c, 0, l, 0, 0, X)) return rc;
+  CK(cudaEventRecord(c->xev[1], X));
+  launch_timed(c, 0, pi);
+  CK(cudaStreamWaitEvent(S, c->xev[1], 0));
+  if (c->prm.use_tvb) launch_timed(c, 1, pb);
+  k = c->xcount++;
+  if (int rc = xpack(c, 1, l, p.write_par, p.write_slot, S, k)) return rc;
+  CK(cudaEventRecord(c->xev[2], S));
+  CK(cudaStreamWaitEvent(X, c->xev[2], 0));
+  if (int rc = xtransfer(c, 1, l, X, k)) return rc;
+  if (int rc = xunpack(c, 1, l, p.write_par, p.write_slot, X)) return rc;
+  CK(cudaEventRecord(c->xev[3], X));
+  if (c->prm.use_tvb) launch_timed(c, 1, pi);
+  CK(cudaStreamWaitEvent(S, c->xev[3], 0));
+  if (int rc = record_dec(c, p.k0, p.k1)) return rc;
+  commit_update(c, l, t, p);
   return SWE_OK;
 }
 
 // Alg. 2 line 1 on every owned element, then the full halo exchange.
 static int group_init_limit(std::vector<Ctx *> &G) {
+  for (Ctx *c : G) {  // the initial limiting is the first record of the decision log (A26)
+    c->declog.clear();
+    c->ndec = 0;
+  }
   for (Ctx *c : G) {
     StepParams p = base_params(c);
     p.k0 = 0;
@@ -1188,25 +1494,49 @@ static int group_init_limit(std::vector<Ctx *> &G) {
     launch(0, true, c->N, p, c->stream, c->f32);
     CK(cudaGetLastError());
   }
-  for (Ctx *c : G)
-    if (int rc = xpack(c, 0, 0, 0, 0)) return rc;
-  for (Ctx *c : G)
-    if (int rc = xtransfer(c, 0, 0)) return rc;
-  for (Ctx *c : G)
-    if (int rc = xunpack(c, 0, 0, 0, 0)) return rc;
+  if (int rc = group_exchange(G, 0, 0, 0, 0)) return rc;
   for (Ctx *c : G)
     if (c->prm.use_tvb) launch(1, false, c->N, c->cur, c->stream, c->f32);
+  if (int rc = group_exchange(G, 1, 0, 0, -1)) return rc;
   for (Ctx *c : G)
-    if (int rc = xpack(c, 1, 0, 0, -1)) return rc;
-  for (Ctx *c : G)
-    if (int rc = xtransfer(c, 1, 0)) return rc;
-  for (Ctx *c : G)
-    if (int rc = xunpack(c, 1, 0, 0, -1)) return rc;
+    if (int rc = record_dec(c, 0, c->kown)) return rc;
+  return SWE_OK;
+}
+
+// Global minimum of r_min over every rank through the IPC blocks (the r_min words have their own flag
+// pair, counted per binning: a rank can be at most one binning ahead of any other).
+static int ipc_rmin(Ctx *c) {
+  const long n = c->rcount++;
+  const int sl = (int)(n & 1);
+  const cuuint64_t v = (cuuint64_t)n + 1;
+  cudaStream_t S = c->stream;
+  CK(cudaMemcpyAsync(c->ipcBlock + 32 + 8 * sl, c->dRmin, sizeof(double), cudaMemcpyDeviceToDevice, S));
+  if (g_write64((CUstream)S, (CUdeviceptr)(c->ipcBlock + 16 + 8 * sl), v, 0) != CUDA_SUCCESS) {
+    c->err = "cuStreamWriteValue64 failed";
+    return SWE_ERR_CUDA;
+  }
+  std::vector<double> r((size_t)c->nranks, std::numeric_limits<double>::infinity());
+  for (int q = 0; q < c->nranks; q++) {
+    char *pb = q == c->rank ? c->ipcBlock : c->ipcPeer[q];
+    if (q != c->rank &&
+        g_wait64((CUstream)S, (CUdeviceptr)(pb + 16 + 8 * sl), v, CU_STREAM_WAIT_VALUE_GEQ | g_wait_flush) !=
+            CUDA_SUCCESS) {
+      c->err = "cuStreamWaitValue64 failed";
+      return SWE_ERR_CUDA;
+    }
+    CK(cudaMemcpyAsync(&r[q], pb + 32 + 8 * sl, sizeof(double), cudaMemcpyDeviceToHost, S));
+  }
+  CK(cudaStreamSynchronize(S));
+  double m = r[0];
+  for (double x : r) m = std::min(m, x);
+  CK(cudaMemcpyAsync(c->dRmin, &m, sizeof(double), cudaMemcpyHostToDevice, S));
+  CK(cudaStreamSynchronize(S));
   return SWE_OK;
 }
 
 // r_min over all ranks (levels are global, reading A19)
 static int group_bin(std::vector<Ctx *> &G, int nlevels) {
+  Nvtx range("level binning + initial limiting");
   // r_min on the device, reduced over the group's contexts and over NCCL ranks
   const double inf = std::numeric_limits<double>::infinity();
   double rmin = inf;
@@ -1218,6 +1548,8 @@ static int group_bin(std::vector<Ctx *> &G, int nlevels) {
     CK(cudaGetLastError());
     if (G.size() == 1 && c->comm)  // global minimum across NCCL ranks
       NK(ncclAllReduce(c->dRmin, c->dRmin, 1, ncclDouble, ncclMin, c->comm, c->stream));
+    if (G.size() == 1 && c->ipc)  // across CUDA-IPC ranks
+      if (int rc = ipc_rmin(c)) return rc;
     double r = inf;
     CK(cudaMemcpyAsync(&r, c->dRmin, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1249,6 +1581,9 @@ static int group_bin(std::vector<Ctx *> &G, int nlevels) {
 }
 
 static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
+  Nvtx range("swe_step (macro step)");
+  for (Ctx *c : G)
+    if (int rc = check_bnd(c)) return rc;
   for (Ctx *c : G) {
     if (!c->have_state) {
       c->err = "swe_step before swe_set_state";
@@ -1279,8 +1614,11 @@ static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
       }
   }
   Ctx *c0 = G[0];
-  if (G.size() == 1 && c0->nranks <= 1 && !c0->prof && c0->use_graphs) {
+  if (G.size() == 1 && c0->nranks <= 1 && !c0->prof && c0->use_graphs && !c0->dDec) {
     if (int rc = graph_step(c0)) return rc;
+  } else if (G.size() == 1 && c0->nranks > 1 && (c0->ipc || c0->comm)) {
+    for (auto &st : c0->schedule)
+      if (int rc = rank_update(c0, st.first, c0->tick + st.second)) return rc;
   } else {
     for (auto &st : c0->schedule)
       if (int rc = group_update(G, st.first, c0->tick + st.second)) return rc;
@@ -1291,7 +1629,7 @@ static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
     {
       Ctx *c = c_;
       CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 4 * kSlots, cudaMemcpyDeviceToHost,
+      CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * kCounters * kSlots, cudaMemcpyDeviceToHost,
                          c->stream));
     }
   }
@@ -1307,6 +1645,8 @@ static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
 }
 
 static int ensure_materialized_group(std::vector<Ctx *> &G) {
+  for (Ctx *c : G)
+    if (int rc = check_bnd(c)) return rc;
   bool need = false;
   for (Ctx *c : G) need = need || !c->materialized;
   if (!need) return SWE_OK;
@@ -1432,6 +1772,7 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   int rc = build_mesh(mesh->nverts, mesh->vx, mesh->vy, mesh->nelems, mesh->etov, mesh->vperiodic, c->mesh, &c->err);
   if (rc) return fail(rc);
   apply_boundary_tags(c->mesh, mesh->vbc);
+  for (int8_t t : c->mesh.bc) c->n_dirichlet += t == 2 ? 1 : 0;
   if (!build_refops(N, c->ops, &c->err)) return fail(SWE_ERR_ORDER);
   for (int f = 0; f < 3; f++)
     for (int k = 0; k < c->ops.Nfp; k++)
@@ -1480,10 +1821,10 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
   c->dOpsG = (double *)c->dalloc(sizeof(double) * sops.size());
   std::vector<float> sopsf(sops.begin(), sops.end());
   c->dOpsGf = (double *)c->dalloc(sizeof(float) * sopsf.size());
-  c->dCounters = (unsigned long long *)c->dalloc(sizeof(unsigned long long) * 4 * kSlots);
+  c->dCounters = (unsigned long long *)c->dalloc(sizeof(unsigned long long) * kCounters * kSlots);
   c->dInjected = (double *)c->dalloc(sizeof(double) * kSlots);
   if (!c->alloc_ok) return fail(SWE_ERR_NOMEM);
-  if (cudaMallocHost(&c->hCounters, sizeof(unsigned long long) * 4 * kSlots) != cudaSuccess) return fail(SWE_ERR_CUDA);
+  if (cudaMallocHost(&c->hCounters, sizeof(unsigned long long) * kCounters * kSlots) != cudaSuccess) return fail(SWE_ERR_CUDA);
   if (cudaMallocHost(&c->hInjected, sizeof(double) * kSlots) != cudaSuccess) return fail(SWE_ERR_CUDA);
   std::vector<double> wm2(c->Np);
   for (int i = 0; i < c->Np; i++) wm2[i] = 0.5 * c->ops.wmean[i];
@@ -1496,7 +1837,7 @@ int swe_create(const swe_mesh *mesh, const double *B, int N, double g, const swe
           cudaSuccess ||
       cudaMemcpyAsync(c->dOpsGf, sopsf.data(), sizeof(float) * sopsf.size(), cudaMemcpyHostToDevice, c->stream) !=
           cudaSuccess ||
-      cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * kCounters * kSlots, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream) != cudaSuccess ||
       cudaStreamSynchronize(c->stream) != cudaSuccess) {
     c->err = "initial upload failed";
@@ -1526,7 +1867,7 @@ int swe_set_state(swe_ctx *h, const double *hh, const double *hu, const double *
   k_speeds<<<(c->Kin + 127) / 128, 128, 0, c->stream>>>(c->Kin, c->Np, c->g, e4, c->prm.a_floor, c->dStage,
                                                          c->dStage + KNp, c->dStage + 2 * KNp, c->dAe);
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
+  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * kCounters * kSlots, c->stream));
   CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream));
   c->have_state = true;
   c->materialized = false;
@@ -1534,7 +1875,30 @@ int swe_set_state(swe_ctx *h, const double *hh, const double *hu, const double *
   c->n_updates = 0;
   c->tick = 0;
   c->t_base = 0.0;
+  c->declog.clear();
+  c->ndec = 0;
   return SWE_OK;
+}
+
+int swe_set_boundary_state(swe_ctx *h, const double *hh, const double *hu, const double *hv) {
+  if (!h || !hh || !hu || !hv) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  const size_t KNp = (size_t)c->Kin * c->Np;
+  if (!c->dBndStage) {
+    c->dBndStage = (double *)c->dalloc(sizeof(double) * 3 * KNp);
+    c->dQbnd = (double *)c->dalloc(c->esz * 3 * c->Np * eb_pad((size_t)c->K));
+    c->dBmean = (double *)c->dalloc(c->esz * 3 * eb_pad((size_t)c->K));
+    if (!c->alloc_ok) {
+      c->alloc_ok = true;
+      c->err = "swe_set_boundary_state: device allocation failed";
+      return SWE_ERR_NOMEM;
+    }
+  }
+  CK(cudaMemcpyAsync(c->dBndStage, hh, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dBndStage + KNp, hu, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dBndStage + 2 * KNp, hv, sizeof(double) * KNp, cudaMemcpyHostToDevice, c->stream));
+  c->bnd_set = true;
+  return scatter_bnd(c);
 }
 
 int swe_step(swe_ctx *h, double dt, int nlevels) {
@@ -1595,13 +1959,15 @@ int swe_regroup(swe_ctx *h) {
   k_speeds<<<(c->Kin + 127) / 128, 128, 0, c->stream>>>(c->Kin, c->Np, c->g, e4, c->prm.a_floor, c->dStage,
                                                          c->dStage + KNp, c->dStage + 2 * KNp, c->dAe);
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * 4 * kSlots, c->stream));
+  CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * kCounters * kSlots, c->stream));
   CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream));
   c->materialized = false;
   c->scheduled = false;
   c->n_updates = 0;
   c->tick = 0;
   c->t_base = t;
+  c->declog.clear();
+  c->ndec = 0;
   return SWE_OK;
 }
 
@@ -1615,8 +1981,15 @@ int swe_get_state(swe_ctx *h, double *hh, double *hu, double *hv) {
   int rc = ensure_materialized_group(G);
   if (rc) return rc;
   const size_t KNp = (size_t)c->Kin * c->Np;
-  double *tmp = (double *)c->dalloc(sizeof(double) * 3 * KNp);
-  if (!tmp) return SWE_ERR_NOMEM;
+  if (!c->dGather) {
+    c->dGather = (double *)c->dalloc(sizeof(double) * 3 * KNp);
+    if (!c->dGather) {
+      c->alloc_ok = true;  // a later call may retry
+      c->err = "swe_get_state: device allocation failed";
+      return SWE_ERR_NOMEM;
+    }
+  }
+  double *tmp = c->dGather;
   GatherParams g = gather_params(c, tmp, tmp + KNp, tmp + 2 * KNp);
   if (c->f32)
     k_gather_state<float><<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
@@ -1642,7 +2015,6 @@ int swe_get_state(swe_ctx *h, double *hh, double *hu, double *hv) {
       }
     }
   }
-  c->dfree(tmp);
   if (e != cudaSuccess) return cuda_fail(c, e, "swe_get_state");
   return SWE_OK;
 }
@@ -1651,17 +2023,25 @@ void swe_destroy(swe_ctx *h) {
   if (!h) return;
   Ctx *c = &h->c;
   if (c->stream || c->dQ) cudaStreamSynchronize(c->stream);
+  if (c->cstream) {
+    cudaStreamSynchronize(c->cstream);
+    cudaStreamDestroy(c->cstream);
+  }
+  for (cudaEvent_t e : c->xev)
+    if (e) cudaEventDestroy(e);
+  for (char *pb : c->ipcPeer)
+    if (pb) cudaIpcCloseMemHandle(pb);
+  if (c->ipcBlock) cudaFree(c->ipcBlock);
   if (c->comm) ncclCommDestroy(c->comm);
-  for (Ctx *q : c->group)
-    if (q && q != c) {
-      auto &gq = q->group;
-      for (auto &p : gq)
-        if (p == c) p = nullptr;
-    }
+  // destroying one member unlinks the whole in-process group: the survivors become unlinked
+  // contexts (their next step reports the missing transport instead of touching a freed peer)
+  const std::vector<Ctx *> members = c->group;
+  for (Ctx *q : members)
+    if (q && q != c) q->group.clear();
   void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo,
                   c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG, c->dOpsGf, c->dHk, c->dLev, c->dLevRes, c->dFlag,
-                  c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXsIdx,
-                  c->dXrIdx,   c->dDry,   c->dCounters};
+                  c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXidx,
+                  c->dDry,   c->dCounters, c->dGather, c->dDec, c->dBndStage, c->dQbnd, c->dBmean};
   clear_graphs(c);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->gev0) cudaEventDestroy(c->gev0);
@@ -1716,7 +2096,7 @@ int swe_get_info(swe_ctx *h, swe_info *info) {
   std::vector<double> part(2 * (size_t)nb);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(part.data(), c->dPartials, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * 4 * kSlots, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hCounters, c->dCounters, sizeof(unsigned long long) * kCounters * kSlots, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(c->hInjected, c->dInjected, sizeof(double) * kSlots, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   double mass = 0.0, mn = 1e300;
@@ -1732,10 +2112,126 @@ int swe_get_info(swe_ctx *h, swe_info *info) {
   info->n_pp = (int64_t)counter(c, 0);
   info->n_dry = (int64_t)counter(c, 1);
   info->n_tvb = (int64_t)counter(c, 2);
+  info->n_posfix = (int64_t)counter(c, 4);
+  info->n_tvb_cw = (int64_t)counter(c, 5);
   return SWE_OK;
 }
 
 const char *swe_last_error(const swe_ctx *h) { return h ? h->c.err.c_str() : "null context"; }
+
+// ---- CUDA-IPC transport: exchange-block handles
+namespace {
+struct IpcBlobHdr {
+  uint32_t magic, version;
+  int32_t rank, nranks;
+  uint64_t slot_bytes;
+  cudaIpcMemHandle_t handle;
+};  // followed by int64 baseA[nranks], baseB[nranks]
+constexpr uint32_t kIpcMagic = 0x53574531u;  // "SWE1"
+size_t ipc_blob_bytes(int nranks) { return sizeof(IpcBlobHdr) + 2 * sizeof(int64_t) * (size_t)nranks; }
+}  // namespace
+
+int swe_ipc_handle(swe_ctx *h, void *blob, size_t *bytes) {
+  if (!h || !bytes) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  const size_t need = ipc_blob_bytes(c->nranks);
+  if (!blob) {
+    *bytes = need;
+    return SWE_OK;
+  }
+  if (*bytes < need) return SWE_ERR_ARG;
+  if (c->nranks <= 1) {
+    c->err = "swe_ipc_handle: single-rank context";
+    return SWE_ERR_ARG;
+  }
+  if (!c->ipcBlock) {  // plain cudaMalloc (IPC-exportable), not the caller's allocator
+    c->ipcSlotBytes = (c->esz * c->capS + 255) / 256 * 256;
+    void *p = nullptr;
+    CK(cudaMalloc(&p, kIpcHdr + 2 * c->ipcSlotBytes));
+    c->ipcBlock = (char *)p;
+    CK(cudaMemset(c->ipcBlock, 0, kIpcHdr));
+  }
+  IpcBlobHdr hd;
+  std::memset(&hd, 0, sizeof(hd));
+  hd.magic = kIpcMagic;
+  hd.version = 1;
+  hd.rank = c->rank;
+  hd.nranks = c->nranks;
+  hd.slot_bytes = c->ipcSlotBytes;
+  CK(cudaIpcGetMemHandle(&hd.handle, c->ipcBlock));
+  std::vector<int64_t> base((size_t)2 * c->nranks, -1);
+  int64_t oa = 0, ob = 0;
+  for (size_t i = 0; i < c->plan.peers.size(); i++) {  // send layout [peer][level]: peer i's block start
+    base[(size_t)c->plan.peers[i]] = oa;
+    base[(size_t)c->nranks + c->plan.peers[i]] = ob;
+    oa += (int64_t)c->sendA[i].size();
+    ob += (int64_t)c->sendB[i].size();
+  }
+  std::memcpy(blob, &hd, sizeof(hd));
+  std::memcpy((char *)blob + sizeof(hd), base.data(), sizeof(int64_t) * base.size());
+  *bytes = need;
+  return SWE_OK;
+}
+
+int swe_ipc_open(swe_ctx *h, const void *blobs) {
+  if (!h || !blobs) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  if (!c->ipcBlock) {
+    c->err = "swe_ipc_open before swe_ipc_handle";
+    return SWE_ERR_STATE;
+  }
+  if (int rc = memops_init(c)) return rc;
+  const size_t bb = ipc_blob_bytes(c->nranks);
+  c->ipcPeer.assign((size_t)c->nranks, nullptr);
+  c->ipcPeerSlot.assign((size_t)c->nranks, 0);
+  c->ipcBaseA.assign(c->plan.peers.size(), 0);
+  c->ipcBaseB.assign(c->plan.peers.size(), 0);
+  for (int q = 0; q < c->nranks; q++) {
+    const char *b = (const char *)blobs + bb * (size_t)q;
+    IpcBlobHdr hd;
+    std::memcpy(&hd, b, sizeof(hd));
+    if (hd.magic != kIpcMagic || hd.version != 1 || hd.rank != q || hd.nranks != c->nranks) {
+      c->err = "swe_ipc_open: blob " + std::to_string(q) + " is not rank " + std::to_string(q) + "'s handle";
+      return SWE_ERR_ARG;
+    }
+    const int64_t *base = (const int64_t *)(b + sizeof(hd));
+    bool peer = false;
+    for (size_t i = 0; i < c->plan.peers.size(); i++)
+      if (c->plan.peers[i] == q) {
+        peer = true;
+        c->ipcBaseA[i] = base[c->rank];
+        c->ipcBaseB[i] = base[c->nranks + c->rank];
+      }
+    if (peer != (base[c->rank] >= 0)) {
+      c->err = "swe_ipc_open: halo plans of ranks " + std::to_string(c->rank) + " and " + std::to_string(q) + " disagree";
+      return SWE_ERR_MESH;
+    }
+    c->ipcPeerSlot[(size_t)q] = (size_t)hd.slot_bytes;
+    if (q == c->rank) continue;
+    void *p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, hd.handle, cudaIpcMemLazyEnablePeerAccess));
+    c->ipcPeer[(size_t)q] = (char *)p;
+  }
+  c->ipc = true;
+  return SWE_OK;
+}
+
+int swe_get_decisions(swe_ctx *h, uint8_t *log, int64_t *nrec) {
+  if (!h || !nrec) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  if (!c->prm.record_decisions) {
+    c->err = "swe_get_decisions: record_decisions is off";
+    return SWE_ERR_STATE;
+  }
+  if (!log) {
+    *nrec = c->ndec;
+    return SWE_OK;
+  }
+  const int64_t n = std::max<int64_t>(0, std::min<int64_t>(*nrec, c->ndec));
+  std::memcpy(log, c->declog.data(), (size_t)n * (size_t)c->Kin);
+  *nrec = n;
+  return SWE_OK;
+}
 
 int swe_profile(swe_ctx *h, int on) {
   if (!h) return SWE_ERR_ARG;

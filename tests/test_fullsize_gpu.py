@@ -60,3 +60,72 @@ def test_c5_fullsize_lake_at_rest(c5):
     assert np.abs(hh + Bw).max() <= 1e-12 * 4100.0
     assert max(np.abs(mu).max(), np.abs(mv).max()) <= 1e-10 * 4100.0 * np.sqrt(9.81 * 4100.0)
     assert s.info()["n_tvb"] == 0
+
+
+def _replayed_parity(w, nsteps, dt, nlevels, **over):
+    """GPU run with the decision log, the oracle replaying it, element-wise parity."""
+    m = w.mesh
+    oracle.set_threads(0)
+    Np = (w.N + 1) * (w.N + 2) // 2
+    probe = oracle.Oracle(m.vx, m.vy, m.etov, np.zeros((m.K, Np)), w.N, w.g, vper=m.vper)
+    x, y = probe.nodes()
+    del probe
+    B, h, hu, hv = w.fields(x, y)
+    prm = dict(w.params)
+    prm.update(over)
+    s = P.Solver(m.vx, m.vy, m.etov, B, w.N, w.g, vper=m.vper, params=dict(prm, record_decisions=1))
+    s.set_state(h, hu, hv)
+    for _ in range(nsteps):
+        s.step(dt, nlevels)
+    o = oracle.Oracle(m.vx, m.vy, m.etov, B, w.N, w.g, vper=m.vper, **prm)
+    o.set_replay(s.decisions())
+    o.set_state(h, hu, hv)
+    for _ in range(nsteps):
+        assert o.step(dt, nlevels) == 0
+    io, ig = o.info(), s.info()
+    assert io["n_mismatch"] == 0, io
+    assert np.array_equal(o.levels(), s.levels())
+    rel = parity_rel(s.get_state(), o.get_state(), w.g)
+    assert max(rel) <= 1e-12, rel
+    for k in ("n_pp", "n_dry", "n_tvb", "n_posfix"):
+        assert io[k] == ig[k], (k, io[k], ig[k])
+    print(w.name, "levels", np.bincount(s.levels())[1:].tolist(), "rel", rel, "adopted", io["n_adopted"],
+          {k: io[k] for k in ("n_pp", "n_dry", "n_tvb", "n_posfix")})
+    io["levels_used"] = len(np.unique(s.levels()))
+    return io
+
+
+def test_c4_fullsize_100_macro_steps():
+    """North_star: parity after 100 steps.  C4 at full size (187,560 triangles, N = 3, 3 MRAB levels,
+    wet/dry dam break, PP + TVB), 100 macro steps (400 finest substeps)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    w = si.c4_dambreak(N=3, base=1)
+    assert w.mesh.K == 187560
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    io = _replayed_parity(w, 100, dt, 3)
+    assert io["n_pp"] > 0 and io["n_dry"] > 0 and io["levels_used"] == 3
+
+
+def test_c5_base320_100_macro_steps():
+    """C5 recipe at base_n = 320 (446,080 triangles, N = 3, 4 MRAB levels, PP + TVB), 100 macro steps."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    w = si.c5_tsunami(P=1, base_n=320)
+    dt = si.dt_for(w.mesh, w.N, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
+    io = _replayed_parity(w, 100, dt, 4)
+    assert io["n_pp"] > 0 and io["levels_used"] == 4
+
+
+def test_periodic_vortex_mrab_100_macro_steps():
+    """MRAB on a periodic mesh: the C2 vortex (N = 3, no limiters) on a graded periodic 2 x 16 x 16 mesh whose
+    element sizes span 4x, so 3 levels are binned; 100 macro steps; the dense output crosses periodic faces."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    w = si.c2_vortex_graded(3, 16)
+    dt = si.dt_for(w.mesh, 3, w.g, 1.0, 0.0, 0.1, u_max=2.0)
+    io = _replayed_parity(w, 100, dt, 3)
+    assert io["levels_used"] == 3

