@@ -326,6 +326,7 @@ struct Ctx {
   // AB ramp (ring slot mod 3, Q parity mod 2), so each distinct parameter sequence is captured once
   struct StepGraph {
     std::vector<StepParams> seq;
+    long kmod = 0;  // multi-rank: exchange count mod 4 at the step start (the flag values baked into the graph)
     cudaGraphExec_t exec = nullptr;
   };
   std::vector<StepGraph> graphs;
@@ -476,6 +477,28 @@ static cudaError_t upload_ops_any(const RefOps &o) {
   return cudaErrorInvalidValue;
 }
 
+// Launch with programmatic stream serialization (K1_PDL): the kernel may start while the previous kernel in the
+// stream drains; it calls griddep_wait() before reading anything that kernel wrote.
+template <typename P>
+static void launch_pdl(void (*kern)(P), int grid, int block, size_t smem, cudaStream_t s, const P &p) {
+#if K1_PDL
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, p);
+#else
+  kern<<<grid, block, smem, s>>>(p);
+#endif
+}
+
 template <int N, bool INIT, typename T>
 static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
@@ -500,8 +523,8 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
     // function attributes are per device: set them on every launch that needs more than the 48 KB default
     if (smem_mma > 48 * 1024)
       cudaFuncSetAttribute(k_rhs_update_mma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mma);
-    k_rhs_update_mma<N><<<(n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem_mma, s>>>(
-        reinterpret_cast<const StepParams &>(p));
+    launch_pdl(k_rhs_update_mma<N>, (n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem_mma, s,
+               reinterpret_cast<const StepParams &>(p));
     return;
   }
 #if K1_CARVEOUT >= 0
@@ -509,7 +532,10 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   // own-state re-reads and the neighbour gathers
   cudaFuncSetAttribute(k_rhs_update<N, INIT, T>, cudaFuncAttributePreferredSharedMemoryCarveout, K1_CARVEOUT);
 #endif
-  k_rhs_update<N, INIT, T><<<grid, K1_BLOCK, smem, s>>>(p);
+  if (INIT)
+    k_rhs_update<N, INIT, T><<<grid, K1_BLOCK, smem, s>>>(p);
+  else
+    launch_pdl(k_rhs_update<N, INIT, T>, grid, K1_BLOCK, smem, s, p);
 }
 template <int N, typename T>
 static void launch_k2(const StepParamsT<T> &p, cudaStream_t s) {
@@ -518,7 +544,7 @@ static void launch_k2(const StepParamsT<T> &p, cudaStream_t s) {
 #if K2_CARVEOUT >= 0
   cudaFuncSetAttribute(k_tvb<N, T>, cudaFuncAttributePreferredSharedMemoryCarveout, K2_CARVEOUT);
 #endif
-  k_tvb<N, T><<<(n + K2_BLOCK - 1) / K2_BLOCK, K2_BLOCK, 0, s>>>(p);
+  launch_pdl(k_tvb<N, T>, (n + K2_BLOCK - 1) / K2_BLOCK, K2_BLOCK, 0, s, p);
 }
 template <typename T>
 static void launch_t(int which, bool init, int N, const StepParamsT<T> &p, cudaStream_t s) {
@@ -846,8 +872,10 @@ static int memops_init(Ctx *c) {
 }
 // flag value of exchange k in the parity word k mod 2.  A rank writes value(k+2) into that word only after
 // it has waited for every peer's value(k+1), which each peer writes after its own wait on value(k) has
-// passed: an equality wait can therefore never miss its value.
-static cuuint64_t flag_value(long k) { return (cuuint64_t)(k % (1L << 40)) + 1; }
+// passed: an equality wait can therefore never miss its value, and it only needs value(k) != value(k-2).
+// Values cycle with period 4, so a captured macro step (2 exchanges per update, 2 (2^L - 1) per step) replays
+// with the same values every other step (CUDA graphs, graph_step).
+static cuuint64_t flag_value(long k) { return (cuuint64_t)(k & 3) + 1; }
 
 // transfer of exchange k (NCCL point-to-point, in-process peers, or CUDA IPC), enqueued on stream s
 static int xtransfer(Ctx *c, int phase, int lvl, cudaStream_t s, long k) {
@@ -1227,9 +1255,10 @@ static StepParams update_params(Ctx *c, int l, long t) {
   return p;
 }
 
-static void launch_timed(Ctx *c, int which, const StepParams &p) {
+static void launch_timed(Ctx *c, int which, const StepParams &p, cudaStream_t s = nullptr) {
   const int nel = p.k1 - p.k0;
   if (nel <= 0) return;
+  if (!s) s = c->stream;
   if (c->prof) {
     while (c->evpool.size() < c->evnext + 2) {
       cudaEvent_t e;
@@ -1238,16 +1267,16 @@ static void launch_timed(Ctx *c, int which, const StepParams &p) {
     }
     cudaEvent_t e0 = c->evpool[c->evnext], e1 = c->evpool[c->evnext + 1];
     c->evnext += 2;
-    cudaEventRecord(e0, c->stream);
-    launch(which, false, c->N, p, c->stream, c->f32);
-    cudaEventRecord(e1, c->stream);
+    cudaEventRecord(e0, s);
+    launch(which, false, c->N, p, s, c->f32);
+    cudaEventRecord(e1, s);
     c->ev.push_back(e0);
     c->ev.push_back(e1);
     c->evwhich.push_back(which);
     c->prof_bytes[which] += (which == 0 ? k1_bytes(c->N, p.nab, c->prm.use_tvb, c->esz) : k2_bytes(c->esz)) * nel;
     c->prof_launch[which]++;
   } else {
-    launch(which, false, c->N, p, c->stream, c->f32);
+    launch(which, false, c->N, p, s, c->f32);
   }
 }
 
@@ -1295,30 +1324,49 @@ static std::vector<StepParams> next_step_params(Ctx *c) {
   return seq;
 }
 
-static Ctx::StepGraph *find_graph(Ctx *c, const std::vector<StepParams> &seq) {
+static long step_kmod(const Ctx *c, long k0) { return c->nranks > 1 ? (k0 & 3) : 0; }
+
+static Ctx::StepGraph *find_graph(Ctx *c, const std::vector<StepParams> &seq, long kmod) {
   for (auto &g : c->graphs)
-    if (g.seq.size() == seq.size() && std::memcmp(g.seq.data(), seq.data(), sizeof(StepParams) * seq.size()) == 0)
+    if (g.kmod == kmod && g.seq.size() == seq.size() &&
+        std::memcmp(g.seq.data(), seq.data(), sizeof(StepParams) * seq.size()) == 0)
       return &g;
   return nullptr;
 }
 
-static int capture_graph(Ctx *c, std::vector<StepParams> seq) {
-  CK(cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeThreadLocal));
-  for (const StepParams &p : seq) {
-    if (p.k1 > p.k0) {
-      launch(0, false, c->N, p, c->gstream, c->f32);
-      if (c->prm.use_tvb) launch(1, false, c->N, p, c->gstream, c->f32);
-    }
+static int enqueue_rank_update(Ctx *c, const StepParams &p, int l, long k, cudaStream_t S);
+static int ensure_comm_stream(Ctx *c);
+
+// The launches of one macro step (no bookkeeping) on stream S: single rank K1 + K2 per update; a rank of a
+// CUDA-IPC partition the overlapped sequence of rank_update with exchanges k0, k0 + 1, ...
+static int enqueue_step(Ctx *c, const std::vector<StepParams> &seq, long k0, cudaStream_t S) {
+  if (c->nranks <= 1) {
+    for (const StepParams &p : seq)
+      if (p.k1 > p.k0) {
+        launch(0, false, c->N, p, S, c->f32);
+        if (c->prm.use_tvb) launch(1, false, c->N, p, S, c->f32);
+      }
+    return SWE_OK;
   }
+  for (size_t i = 0; i < seq.size(); i++)
+    if (int rc = enqueue_rank_update(c, seq[i], c->schedule[i].first, k0 + 2 * (long)i, S)) return rc;
+  return SWE_OK;
+}
+
+static int capture_graph(Ctx *c, std::vector<StepParams> seq, long k0) {
+  CK(cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeThreadLocal));
+  const int erc = enqueue_step(c, seq, k0, c->gstream);
   cudaGraph_t graph = nullptr;
   const cudaError_t le = cudaGetLastError();
   const cudaError_t ee = cudaStreamEndCapture(c->gstream, &graph);  // always ends the capture
-  if (le != cudaSuccess || ee != cudaSuccess) {
+  if (erc || le != cudaSuccess || ee != cudaSuccess) {
     if (graph) cudaGraphDestroy(graph);
+    if (erc) return erc;
     return cuda_fail(c, le != cudaSuccess ? le : ee, "graph capture");
   }
   Ctx::StepGraph g;
   g.seq = std::move(seq);
+  g.kmod = step_kmod(c, k0);
   cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
@@ -1339,20 +1387,18 @@ static int graph_step(Ctx *c) {
     CK(cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->gev1, cudaEventDisableTiming));
   }
+  if (c->nranks > 1)
+    if (int rc = ensure_comm_stream(c)) return rc;
   const bool after_ramp = ramp_done(c);
+  const long k0 = c->xcount, kstep = c->nranks > 1 ? 2 * (long)c->schedule.size() : 0;
   std::vector<StepParams> seq = next_step_params(c);
   c->cur = seq.back();
-  Ctx::StepGraph *g = find_graph(c, seq);
+  c->xcount += kstep;
+  Ctx::StepGraph *g = find_graph(c, seq, step_kmod(c, k0));
   if (!g) {
-    if (c->graphs.size() >= kMaxGraphs) {  // cache full: launch eagerly
-      for (const StepParams &p : seq)
-        if (p.k1 > p.k0) {
-          launch(0, false, c->N, p, c->stream, c->f32);
-          if (c->prm.use_tvb) launch(1, false, c->N, p, c->stream, c->f32);
-        }
-      return SWE_OK;
-    }
-    if (int rc = capture_graph(c, seq)) return rc;
+    if (c->graphs.size() >= kMaxGraphs)  // cache full: launch eagerly
+      return enqueue_step(c, seq, k0, c->stream);
+    if (int rc = capture_graph(c, seq, k0)) return rc;
     g = &c->graphs.back();
     if (after_ramp) {
       // the launch sequence is periodic (ring slot mod 3, parity mod 2): capture the next five
@@ -1366,13 +1412,14 @@ static int graph_step(Ctx *c) {
       for (int k = 0; k < 5 && c->graphs.size() < kMaxGraphs; k++) {
         c->tick += 1L << (c->L - 1);
         std::vector<StepParams> s2 = next_step_params(c);
-        if (!find_graph(c, s2))
-          if (int rc = capture_graph(c, std::move(s2))) return rc;
+        const long k2 = k0 + (k + 1) * kstep;
+        if (!find_graph(c, s2, step_kmod(c, k2)))
+          if (int rc = capture_graph(c, std::move(s2), k2)) return rc;
       }
       for (int l = 0; l <= 8; l++) c->par[l] = par[l], c->kcount[l] = kc[l], c->tick_s[l] = ts[l], c->t_e[l] = te[l];
       c->tick = tick;
       c->n_updates = nup;
-      g = find_graph(c, seq);
+      g = find_graph(c, seq, step_kmod(c, k0));
     }
   }
   CK(cudaEventRecord(c->gev0, c->stream));  // the step starts after the caller's prior work
@@ -1444,35 +1491,42 @@ static int ensure_comm_stream(Ctx *c) {
 //   comm:                         | exchange A     |                               | exchange B     |
 // Interior elements have no ghost neighbour, so K1(interior) does not read what exchange B of the previous
 // update delivers, and neither interior kernel touches a ghost.
-static int rank_update(Ctx *c, int l, long t) {
-  Nvtx range(kLevelRange[l]);
+// The launches of one such update on compute stream S (eager: the context's stream; graph capture: the capture
+// stream), exchanges k and k + 1.
+static int enqueue_rank_update(Ctx *c, const StepParams &p, int l, long k, cudaStream_t S) {
   if (int rc = ensure_comm_stream(c)) return rc;
-  const StepParams p = update_params(c, l, t);
-  c->cur = p;
   StepParams pb = p, pi = p;
   pb.k1 = c->bnd[l];
   pi.k0 = c->bnd[l];
-  cudaStream_t S = c->stream, X = c->cstream;
-  launch_timed(c, 0, pb);
-  long k = c->xcount++;
+  cudaStream_t X = c->cstream;
+  launch_timed(c, 0, pb, S);
   if (int rc = xpack(c, 0, l, 0, 0, S, k)) return rc;
   CK(cudaEventRecord(c->xev[0], S));
   CK(cudaStreamWaitEvent(X, c->xev[0], 0));
   if (int rc = xtransfer(c, 0, l, X, k)) return rc;
   if (int rc = xunpack(c, 0, l, 0, 0, X)) return rc;
   CK(cudaEventRecord(c->xev[1], X));
-  launch_timed(c, 0, pi);
+  launch_timed(c, 0, pi, S);
   CK(cudaStreamWaitEvent(S, c->xev[1], 0));
-  if (c->prm.use_tvb) launch_timed(c, 1, pb);
-  k = c->xcount++;
+  if (c->prm.use_tvb) launch_timed(c, 1, pb, S);
+  k++;
   if (int rc = xpack(c, 1, l, p.write_par, p.write_slot, S, k)) return rc;
   CK(cudaEventRecord(c->xev[2], S));
   CK(cudaStreamWaitEvent(X, c->xev[2], 0));
   if (int rc = xtransfer(c, 1, l, X, k)) return rc;
   if (int rc = xunpack(c, 1, l, p.write_par, p.write_slot, X)) return rc;
   CK(cudaEventRecord(c->xev[3], X));
-  if (c->prm.use_tvb) launch_timed(c, 1, pi);
+  if (c->prm.use_tvb) launch_timed(c, 1, pi, S);
   CK(cudaStreamWaitEvent(S, c->xev[3], 0));
+  return SWE_OK;
+}
+
+static int rank_update(Ctx *c, int l, long t) {
+  Nvtx range(kLevelRange[l]);
+  const StepParams p = update_params(c, l, t);
+  c->cur = p;
+  if (int rc = enqueue_rank_update(c, p, l, c->xcount, c->stream)) return rc;
+  c->xcount += 2;
   if (int rc = record_dec(c, p.k0, p.k1)) return rc;
   commit_update(c, l, t, p);
   return SWE_OK;
@@ -1614,7 +1668,7 @@ static int group_step(std::vector<Ctx *> &G, double dt, int nlevels) {
       }
   }
   Ctx *c0 = G[0];
-  if (G.size() == 1 && c0->nranks <= 1 && !c0->prof && c0->use_graphs && !c0->dDec) {
+  if (G.size() == 1 && (c0->nranks <= 1 || c0->ipc) && !c0->prof && c0->use_graphs && !c0->dDec) {
     if (int rc = graph_step(c0)) return rc;
   } else if (G.size() == 1 && c0->nranks > 1 && (c0->ipc || c0->comm)) {
     for (auto &st : c0->schedule)

@@ -212,7 +212,7 @@ def _ipc_worker(rank, world, port, outdir, case):
     else:  # bench.py's weak-scaling setup: every rank builds only its own C5 strip (+ buffer rows)
         w, owner, gid = si.c5_rank_strip(rank, world, 80)
         m = w.mesh
-        L, nsteps = 4, 3
+        L, nsteps = 4, 8
         full = si.c5_tsunami(P=world, base_n=80, shuffle_seed=None)
         dt = si.dt_for(full.mesh, 3, full.g, 4001.0, full.params["a_floor"], full.dt_factor)
     x, y = P.nodes(m.vx, m.vy, m.etov, w.N)
@@ -240,7 +240,8 @@ def _ipc_worker(rank, world, port, outdir, case):
 def test_ipc_ranks_bit_identical(case, world, tmp_path):
     """The CUDA-IPC transport with one process per rank (all on this box's single GPU): boundary-first
     level updates with the halo exchanges on a communication stream (stream-memory-op flags, peer copies
-    of face traces).  The owned elements must equal a single-rank run bit for bit, levels included."""
+    of face traces), the macro steps after the AB ramp captured as CUDA graphs and replayed.  The owned
+    elements must equal a single-rank run bit for bit, levels included."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     mp.spawn(_ipc_worker, args=(world, _free_port(), str(tmp_path), case), nprocs=world, join=True)
@@ -252,7 +253,7 @@ def test_ipc_ranks_bit_identical(case, world, tmp_path):
     else:
         w = si.c5_tsunami(P=world, base_n=80, shuffle_seed=None)
         m = w.mesh
-        L, nsteps = 4, 3
+        L, nsteps = 4, 8
         dt = si.dt_for(m, 3, w.g, 4001.0, w.params["a_floor"], w.dt_factor)
     x, y = P.nodes(m.vx, m.vy, m.etov, w.N)
     B, h, hu, hv = w.fields(x, y)

@@ -1,6 +1,6 @@
 #!/bin/bash
-# Round profile capture (full-size C5, N=3, L=4): launch list + ncu --set full of K1 (level 4 and level 1
-# launches of macro step 3, AB3 active) and K2.  Kernel launches per macro step: 15 K1 + 15 K2.
+# Round profile capture (full-size C5, N=3, L=4): launch list with per-launch DRAM bytes, ncu --set full of
+# K1 (level-4 and level-1 launches of macro step 3, AB3 active) and of one K2 launch.
 mkdir -p gpurun_out
 B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
@@ -11,5 +11,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:^k_r
    -o gpurun_out/k1_l1 $B > gpurun_out/ncu_k1_l1.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:^k_tvb$ -s 30 -c 1 \
    -o gpurun_out/k2_l4 $B > gpurun_out/ncu_k2.log 2>&1
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_full.log 2>&1
 ls -la gpurun_out
