@@ -46,7 +46,7 @@ def run32(w, nsteps, dt, nlevels=1, **over):
     return o, s, d
 
 
-@pytest.mark.parametrize("N", [1, 2, 3, 4])
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5])
 def test_fp32_vortex_parity(N):
     """Smooth periodic vortex, no limiters (C2 recipe), 60 steps."""
     w = si.c2_vortex(N, 12)

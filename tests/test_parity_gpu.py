@@ -323,6 +323,21 @@ def test_dirichlet_requires_boundary_state():
     assert ei.value.code == -4
 
 
+def test_all_dry_domain():
+    """Degenerate case: no water anywhere (h = 0 at every node over a varying bed).  Alg. 2 line 1 makes
+    every element dry (h = h0), nothing is non-finite, TVB never runs, and the state, the
+    injected mass and the counters agree with the oracle through MRAB steps."""
+    w = si.c4_dambreak(N=3, base=10)
+    w.initial = lambda x, y: (np.zeros_like(x), np.zeros_like(x), np.zeros_like(x))
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    o, s, _ = run_both(w, 5, dt, nlevels=3)
+    io = _counters_equal(o, s)
+    assert io["n_dry"] > 0 and io["n_tvb"] == 0
+    assert_parity(o, s, w.g)
+    h = s.get_state()[0]
+    assert np.all(h == w.params["h0"])
+
+
 def test_mass_conservation_gpu_single_rate():
     w = si.c3_thacker(N=2, n=40)
     o, s, d = make_pair(w)
