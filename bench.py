@@ -432,7 +432,7 @@ def run_rank(args):
             "util_pct_of_theoretical": dram_util, "theoretical_gbs": gpm.theoretical_gbs, "gbs": dram_gbs,
             "frac_of_measured_peak": dram_gbs / peak,
             "bytes_per_elem_update": dram_gbs * 1e9 * (ms_rank / 1e3) / upd if upd else None}
-    traffic_path = os.path.join(ROOT, "profiles", "r02_k1_traffic.json")
+    traffic_path = os.path.join(ROOT, "profiles", "r02b_k1_traffic.json")
     if N == 3 and args.precision == 64 and os.path.exists(traffic_path):
         try:  # K1's own DRAM bytes per launch: ncu --set full capture committed under profiles/ (not this run)
             tr = json.load(open(traffic_path))
