@@ -453,7 +453,7 @@ static std::vector<double> smem_ops(const RefOps &o) {
           v[SO::FP + ((op * SO::NKP + ks) * SO::NTN + nt) * 32 + l] =
               (pt < SO::Nc && node < SO::Np) ? (*pops[op])(node, pt) : 0.0;
         }
-  // lift fragments (K1_MMA2)
+  // lift fragments (k_rhs_update_mma2)
   v.resize(SO::total2, 0.0);
   for (int ks = 0; ks < SO::NKL / 4; ks++)
     for (int nt = 0; nt < SO::NTN; nt++)
@@ -525,21 +525,11 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   }
   grid = std::min(grid, resident);
 #endif
-  if constexpr (!INIT && N >= K1_MMA_MIN_N && sizeof(T) == 8 && K1_MMA2) {  // FP64 tensor path, lift on DMMA
+  if constexpr (!INIT && N >= K1_MMA_MIN_N && sizeof(T) == 8) {  // FP64 tensor path: volume term and lift on DMMA (FP32: scalar path)
     const size_t smem2 = mma2_smem_bytes<N>();
     if (smem2 > 48 * 1024)
       cudaFuncSetAttribute(k_rhs_update_mma2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     launch_pdl(k_rhs_update_mma2<N>, (n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem2, s,
-               reinterpret_cast<const StepParams &>(p));
-    return;
-  }
-  if constexpr (!INIT && N >= K1_MMA_MIN_N && sizeof(T) == 8) {  // FP64 tensor path (FP32: scalar path)
-    const size_t smem_mma =
-        sizeof(double) * (SmemOps<N>::total + (K1_MMA_TILE ? (size_t)(4 * SmemOps<N>::Np + 1) * (K1_BLOCK + kTilePad) : 0));
-    // function attributes are per device: set them on every launch that needs more than the 48 KB default
-    if (smem_mma > 48 * 1024)
-      cudaFuncSetAttribute(k_rhs_update_mma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mma);
-    launch_pdl(k_rhs_update_mma<N>, (n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem_mma, s,
                reinterpret_cast<const StepParams &>(p));
     return;
   }

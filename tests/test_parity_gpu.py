@@ -211,7 +211,7 @@ def test_parity_mrab_dambreak(nlevels):
 
 
 def test_parity_mrab_dambreak_n4_tensor_path():
-    """N = 4 runs the volume term on the FP64 tensor path (DMMA, k_rhs_update_mma): C4 wet/dry with
+    """N = 4 runs the volume term and the lift on the FP64 tensor path (DMMA, k_rhs_update_mma2): C4 wet/dry with
     PP + TVB and 3 MRAB levels against the oracle."""
     w = si.c4_dambreak(N=4, base=5)
     dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
@@ -246,6 +246,28 @@ def test_parity_mrab_dambreak_n5():
     _counters_equal(o, s)
     assert s.info()["n_pp"] > 0
     assert_parity(o, s, w.g)
+
+
+@pytest.mark.parametrize("N", [4, 5])
+def test_tensor_path_is_run_to_run_bit_identical(N):
+    """k_rhs_update_mma2 hands the face fluxes and the RHS between lanes through a shared tile ordered by
+    __syncwarp (compute-sanitizer is not available on this pool): a missing order would show up as a result that
+    changes from run to run.  Two identical runs on a graded wet/dry mesh, 3 levels, must agree bit for bit."""
+    w = si.c4_dambreak(N=N, base=5)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    m = w.mesh
+    x, y = P.nodes(m.vx, m.vy, m.etov, N)
+    B, h, hu, hv = w.fields(x, y)
+    out = []
+    for _ in range(2):
+        s = P.Solver(m.vx, m.vy, m.etov, B, N, w.g, params=w.params)
+        s.set_state(h, hu, hv)
+        for _ in range(6):
+            s.step(dt, 3)
+        out.append(s.get_state())
+        s.close()
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
 
 
 def test_convergence_sweep_n1_to_n5_through_the_abi():
@@ -519,7 +541,7 @@ def test_parity_outflow_boundary():
 
 
 def test_parity_outflow_boundary_tensor_path():
-    """The N = 4 tensor-path K1 (k_rhs_update_mma) with a transmissive outflow boundary (A7')."""
+    """The N = 4 tensor-path K1 (k_rhs_update_mma2) with a transmissive outflow boundary (A7')."""
     w = si.c7_rarefaction_outflow(4, 2, True, t0=4.8)
     dt = si.dt_for(w.mesh, w.N, w.g, 1.0, 0.0, 0.2, u_max=2.0)
     o, s, _ = run_both(w, 80, dt)

@@ -1,5 +1,5 @@
 """Small runs of every kernel path for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
-C1 hump (N = 2, PP + TVB), C4 dam break (N = 3, 3 MRAB levels, graphs), N = 4 (DMMA K1), FP32, a Dirichlet
+C1 hump (N = 2, PP + TVB), C4 dam break (N = 3, 3 MRAB levels, graphs), N = 4 and N = 5 (DMMA K1), FP32, a Dirichlet
 vortex and an in-process 2-rank partition.  Exits non-zero on any solver error.
     compute-sanitizer --tool memcheck python tools/sanitize_run.py"""
 import os
@@ -36,6 +36,8 @@ run(w, 10, si.dt_for(w.mesh, 3, w.g, 1.875, 13.0, 0.2), L=3)  # 10 macro steps: 
 run(w, 3, si.dt_for(w.mesh, 3, w.g, 1.875, 13.0, 0.2), L=3, prm=dict(precision=32))
 w4 = si.c4_dambreak(N=4, base=10)
 run(w4, 3, si.dt_for(w4.mesh, 4, w4.g, 1.875, 13.0, 0.2), L=3)
+w5 = si.c4_dambreak(N=5, base=10)
+run(w5, 3, si.dt_for(w5.mesh, 5, w5.g, 1.875, 13.0, 0.2), L=3)
 wd = si.c2_vortex_dirichlet(2, 8)
 run(wd, 4, si.dt_for(wd.mesh, 2, wd.g, 1.0, 0.0, 0.1, u_max=2.0), bnd=True)
 # in-process 2-rank partition (halo pack / unpack kernels)
