@@ -272,6 +272,9 @@ struct Ctx {
   double *dQ = nullptr, *dR = nullptr, *dB = nullptr, *dV = nullptr, *dMeans = nullptr, *dUT = nullptr;
   double *dTalpha = nullptr, *dTgeo = nullptr, *dGeo = nullptr, *dAe = nullptr, *dStage = nullptr, *dInjected = nullptr, *dWm2 = nullptr;
   double *dBcaller = nullptr, *dPartials = nullptr, *dOpsG = nullptr, *dOpsGf = nullptr, *dRmin = nullptr;
+  int *dK2list = nullptr;             // K2_LIST: elements K1 hands to K2 (single rank)
+  unsigned int *dK2cnt = nullptr;     // [2] list lengths
+  long k2u = 0;                       // list-mode updates so far (the slot of an update is k2u & 1)
   double *dGather = nullptr;             // caller-layout state for swe_get_state (allocated on first use)
   double *dBndStage = nullptr;           // Dirichlet boundary state, caller layout [3][Kin][Np] (A7'')
   double *dQbnd = nullptr, *dBmean = nullptr;  // ... in the internal layout, and its cell means
@@ -550,6 +553,10 @@ static void launch_k2(const StepParamsT<T> &p, cudaStream_t s) {
 #if K2_CARVEOUT >= 0
   cudaFuncSetAttribute(k_tvb<N, T>, cudaFuncAttributePreferredSharedMemoryCarveout, K2_CARVEOUT);
 #endif
+  if (p.k2list) {  // K2_LIST: a grid-stride pass over the list K1 built (its length is known on the device only)
+    launch_pdl(k_tvb_list<N, T>, std::min((n + K2_BLOCK - 1) / K2_BLOCK, K2_LIST_GRID), K2_BLOCK, 0, s, p);
+    return;
+  }
   launch_pdl(k_tvb<N, T>, (n + K2_BLOCK - 1) / K2_BLOCK, K2_BLOCK, 0, s, p);
 }
 template <typename T>
@@ -595,6 +602,7 @@ static StepParamsT<float> to_f32(const StepParams &d) {
   f.use_pp = d.use_pp, f.use_tvb = d.use_tvb;
   f.counters = d.counters, f.injected = d.injected, f.opsG = (const float *)d.opsG, f.dec = d.dec;
   f.Qbnd = (const float *)d.Qbnd, f.bmean = (const float *)d.bmean;
+  f.k2list = d.k2list, f.k2cnt = d.k2cnt, f.k2slot = d.k2slot;
   return f;
 }
 
@@ -680,6 +688,8 @@ static int alloc_state(Ctx *c) {
   if (c->prm.record_decisions) c->dDec = (unsigned char *)c->dalloc(K);
   c->dPartials = (double *)c->dalloc(sizeof(double) * 2 * ((K + 255) / 256));
   c->dRmin = (double *)c->dalloc(sizeof(double));
+  c->dK2list = (int *)c->dalloc(sizeof(int) * K);
+  c->dK2cnt = (unsigned int *)c->dalloc(sizeof(unsigned int) * 2);
   // exchange entry lists (level-independent) and buffer capacities
   build_entry_lists(c);
   size_t nsA = 0, nrA = 0, nsB = 0, nrB = 0;
@@ -1157,6 +1167,8 @@ static int materialize_state(Ctx *c) {
   CK(cudaGetLastError());
   if (int rc = scatter_bnd(c)) return rc;
   CK(cudaMemsetAsync(c->dDry, 0, (size_t)4 * K, c->stream));
+  CK(cudaMemsetAsync(c->dK2cnt, 0, sizeof(unsigned int) * 2, c->stream));
+  c->k2u = 0;
   CK(cudaMemsetAsync(c->dCounters, 0, sizeof(unsigned long long) * kCounters * kSlots, c->stream));
   CK(cudaMemsetAsync(c->dInjected, 0, sizeof(double) * kSlots, c->stream));
   c->n_updates = 0;
@@ -1221,6 +1233,12 @@ static StepParams update_params(Ctx *c, int l, long t) {
   StepParams p = base_params(c);
   p.k0 = c->off[l - 1];
   p.k1 = c->off[l];
+  if (K2_LIST && c->nranks <= 1 && c->group.size() <= 1 && c->prm.use_tvb && p.k1 > p.k0) {
+    // K2 over the list of the update's non-quiet, non-dry elements that K1 appends to
+    p.k2list = c->dK2list;
+    p.k2cnt = c->dK2cnt;
+    p.k2slot = (int)(c->k2u++ & 1);
+  }
   const double dtl = std::ldexp(c->dt, l - 1);
   const int k = c->kcount[l];
   const int m = std::min(k + 1, 3);
@@ -1414,7 +1432,7 @@ static int graph_step(Ctx *c) {
       int kc[9];
       long ts[9], te[9];
       for (int l = 0; l <= 8; l++) kc[l] = c->kcount[l], ts[l] = c->tick_s[l], te[l] = c->t_e[l];
-      const long tick = c->tick, nup = c->n_updates;
+      const long tick = c->tick, nup = c->n_updates, k2u = c->k2u;
       for (int k = 0; k < 5 && c->graphs.size() < kMaxGraphs; k++) {
         c->tick += 1L << (c->L - 1);
         std::vector<StepParams> s2 = next_step_params(c);
@@ -1425,6 +1443,7 @@ static int graph_step(Ctx *c) {
       for (int l = 0; l <= 8; l++) c->par[l] = par[l], c->kcount[l] = kc[l], c->tick_s[l] = ts[l], c->t_e[l] = te[l];
       c->tick = tick;
       c->n_updates = nup;
+      c->k2u = k2u;
       g = find_graph(c, seq, step_kmod(c, k0));
     }
   }
@@ -2101,7 +2120,7 @@ void swe_destroy(swe_ctx *h) {
   void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo,
                   c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG, c->dOpsGf, c->dHk, c->dLev, c->dLevRes, c->dFlag,
                   c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXidx,
-                  c->dDry,   c->dCounters, c->dGather, c->dDec, c->dBndStage, c->dQbnd, c->dBmean};
+                  c->dDry,   c->dCounters, c->dGather, c->dDec, c->dBndStage, c->dQbnd, c->dBmean, c->dK2list, c->dK2cnt};
   clear_graphs(c);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->gev0) cudaEventDestroy(c->gev0);
