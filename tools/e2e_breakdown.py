@@ -41,3 +41,12 @@ print("first step (bin+limit+step) %.1f ms" % t(lambda: s.step(dt, 4)))
 print("steady step                %.1f ms" % t(lambda: s.step(dt, 4), 5))
 print("swe_get_info               %.1f ms" % t(lambda: s.info(), 5))
 print("get_state_into (pinned)    %.1f ms" % t(lambda: s.get_state_into(oh, ohu, ohv)))
+print("get_state_into again       %.1f ms" % t(lambda: s.get_state_into(oh, ohu, ohv)))
+print("set_state again            %.1f ms" % t(lambda: s.set_state(hh, hhu, hhv)))
+print("first step again           %.1f ms" % t(lambda: s.step(dt, 4)))
+# raw PCIe reference: one 565 MB field each way through torch
+a = torch.from_numpy(hh)
+d = torch.empty(a.shape, dtype=a.dtype, device="cuda")
+print("torch H2D one field        %.1f ms (%.1f GB/s)" % (t(lambda: d.copy_(a, non_blocking=True)), 0))
+o = torch.from_numpy(oh)
+print("torch D2H one field        %.1f ms" % t(lambda: o.copy_(d, non_blocking=True)))
