@@ -532,7 +532,8 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
     const size_t smem2 = mma2_smem_bytes<N>();
     if (smem2 > 48 * 1024)
       cudaFuncSetAttribute(k_rhs_update_mma2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-    launch_pdl(k_rhs_update_mma2<N>, (n + K1_BLOCK - 1) / K1_BLOCK, K1_BLOCK, smem2, s,
+    constexpr int bs = mma2_block<N>();
+    launch_pdl(k_rhs_update_mma2<N>, (n + bs - 1) / bs, bs, smem2, s,
                reinterpret_cast<const StepParams &>(p));
     return;
   }

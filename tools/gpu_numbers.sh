@@ -7,3 +7,4 @@ timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_default.log
 for N in 2 4 5; do timeout 600 python bench.py --order $N --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_n$N.log 2>&1; done
 timeout 600 python bench.py --precision 32 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_fp32.log 2>&1
 for f in bench_n2 bench_n4 bench_n5 bench_fp32; do python -c "import json;d=json.loads(open('gpurun_out/$f.log').read().strip().splitlines()[-1]);r=d['roofline'];print('$f', '%.3e'%d['value'], round(r['frac'],3), round(r['step_frac'],3), round(r['k1_launch_ms_avg'],4))"; done
+timeout 900 python bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_gpus2.log 2>&1; tail -1 gpurun_out/bench_gpus2.log | cut -c1-250
