@@ -514,20 +514,9 @@ template <int N, bool INIT, typename T>
 static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
   int n = p.k1 - p.k0;
   if (n <= 0) return;
-  size_t smem = INIT ? 0 : (size_t)k1_ops_bytes<N, T>() + k1_nbr_bytes<N, T>();
+  size_t smem = INIT ? 0 : (size_t)k1_ops_bytes<N, T>();
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_rhs_update<N, INIT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = (n + K1_BLOCK - 1) / K1_BLOCK;
-#if K1_PERSIST
-  int resident = 0;  // SMs x resident blocks per SM (per launch: devices differ)
-  {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update<N, INIT, T>, K1_BLOCK, smem);
-    resident = std::max(1, sms * per_sm);
-  }
-  grid = std::min(grid, resident);
-#endif
   if constexpr (!INIT && N >= K1_MMA_MIN_N && sizeof(T) == 8) {  // FP64 tensor path: volume term and lift on DMMA (FP32: scalar path)
     const size_t smem2 = mma2_smem_bytes<N>();
     if (smem2 > 48 * 1024)
