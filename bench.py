@@ -211,6 +211,66 @@ def cpu_baseline(args, seconds_budget=30.0):
     return out
 
 
+def workloads_table(args, dev):
+    """SURVEY 8(d) "oracle beside it": the CPU oracle and the GPU path on the smaller configs C1-C4 (same inputs, same
+    steps after an untimed start), DOF-updates/s each; bounded so that it adds ~20 s to the run."""
+    import torch
+
+    import oracle
+    import paper_1403_1661_b200 as P
+    import swe_inputs as si
+    cores = oracle.set_threads(0)
+    cases = [
+        ("C1b lake + hump, N=2, 512 el, 1 level", si.c1_lake(N=2, n=16, hump=True), 1, 100,
+         lambda w: si.dt_for(w.mesh, 2, w.g, 1.0, 0.0, 0.2)),
+        ("C2 vortex, N=3, periodic 2x64x64, 1 level", si.c2_vortex(3, 64), 1, 20,
+         lambda w: si.dt_for(w.mesh, 3, 2.0, 1.0, 0.0, 0.1, u_max=2.0)),
+        ("C3 Thacker, N=2, 20k el, PP+TVB, 1 level", si.c3_thacker(N=2, n=100), 1, 20,
+         lambda w: si.dt_for(w.mesh, w.N, w.g, 1.75, 0.0, 0.2, u_max=0.5)),
+        ("C4 dam break, N=3, 188k el, PP+TVB, 3 levels", si.c4_dambreak(N=3, base=1), 3, 3,
+         lambda w: si.dt_for(w.mesh, 3, w.g, 1.875, 13.0, 0.2)),
+    ]
+    rows = []
+    for name, w, L, nsteps, dtf in cases:
+        m = w.mesh
+        Np = (w.N + 1) * (w.N + 2) // 2
+        x, y = P.nodes(m.vx, m.vy, m.etov, w.N)
+        B, h, hu, hv = w.fields(x, y)
+        dt = dtf(w)
+        o = oracle.Oracle(m.vx, m.vy, m.etov, B, w.N, w.g, vper=m.vper, **w.params)
+        o.set_state(h, hu, hv)
+        for _ in range(3):  # past the AB ramp
+            assert o.step(dt, L) == 0
+        U = dof_per_macro_step(o.levels(), L, Np)
+        t0 = time.perf_counter()
+        for _ in range(nsteps):
+            assert o.step(dt, L) == 0
+        t_cpu = time.perf_counter() - t0
+        del o
+        s = P.Solver(m.vx, m.vy, m.etov, B, w.N, w.g, vper=m.vper, params=w.params, device=dev)
+        s.set_state(h, hu, hv)
+        for _ in range(3):
+            s.step(dt, L)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(nsteps):
+            s.step(dt, L)
+        torch.cuda.synchronize()
+        t_gpu = time.perf_counter() - t0
+        s.close()
+        rows.append({"config": name, "elements": int(m.K), "steps": nsteps,
+                     "oracle_dof_per_s": U * nsteps / t_cpu, "gpu_dof_per_s": U * nsteps / t_gpu})
+    cpu_model = ""
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"oracle_cores": cores, "cpu_model": cpu_model, "runs": rows,
+            "note": "wall clock after 3 untimed steps; the small GPU cases are launch-bound (CUDA-graph replay)"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle timed as it stands on the box's host cores."""
     if rank != 0:
@@ -261,6 +321,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-workloads", action="store_true", help="skip the C1-C4 oracle/GPU table")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="halo exchange for N > 1: CUDA-IPC peer copies (default; also ranks sharing a GPU) or NCCL")
     args = ap.parse_args()
@@ -493,6 +554,8 @@ def run_rank(args):
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args)
+        if world == 1 and not args.no_workloads and args.order == 3 and args.precision == 64:
+            cpu["workloads"] = workloads_table(args, dev)
     if rank == 0:
         out = {
             "metric": METRIC.replace("N=3", f"N={N}").replace("FP64", "FP64" if args.precision == 64 else "FP32"),
