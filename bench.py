@@ -537,7 +537,9 @@ def run_rank(args):
                "note": "wall clock, max over ranks: swe_set_state (H2D from pinned memory + level binning + initial "
                        "limiting) once, then per macro step swe_step + swe_get_info (the step's diagnostics D2H), then "
                        "the final state D2H (swe_get_state into pinned memory)"}
-        # secondary: the full state read back after every macro step (output-every-step usage)
+        # secondary: the full state read back after every macro step (output-every-step usage), synchronously
+        # (swe_get_state) and overlapped with the next steps (swe_get_state_async into two pinned buffer sets,
+        # swe_wait_state before the clock stops)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s.set_state(hh, hhu, hhv)
@@ -547,6 +549,20 @@ def run_rank(args):
         torch.cuda.synchronize()
         el2 = time.perf_counter() - t0
         e2e["state_every_step"] = {"value": U_all * k / el2, "d2h_bytes_per_step": int(state_bytes)}
+        if world == 1:
+            ring = [(oh, ohu, ohv), (pin(np.zeros_like(h)), pin(np.zeros_like(h)), pin(np.zeros_like(h)))]
+            s.get_state_async(*ring[1])  # untimed: the snapshot buffers' one-time allocation
+            s.wait_state()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s.set_state(hh, hhu, hhv)
+            for i in range(args.e2e_steps):
+                s.step(dt, L)
+                s.get_state_async(*ring[i % 2])
+            s.wait_state()
+            torch.cuda.synchronize()
+            el3 = time.perf_counter() - t0
+            e2e["state_every_step_async"] = {"value": U_all * k / el3, "d2h_bytes_per_step": int(state_bytes)}
 
     if world > 1:
         torch.distributed.barrier()  # every rank is done with the others' exchange blocks

@@ -160,6 +160,19 @@ int swe_step(swe_ctx *ctx, double dt, int nlevels);
 /* Copy the current state to the host, caller order, [nelems*Np] each. */
 int swe_get_state(swe_ctx *ctx, double *h, double *hu, double *hv);
 
+/* Output while the run goes on: enqueue a copy of the current state (the state after every call made so far) into
+ * h, hu, hv ([nelems*Np] each, caller order) and return without waiting.  The state is first gathered on the device
+ * into one of two context-owned snapshot buffers (3*nelems*Np doubles each, allocated on first use); the device->host
+ * copy then runs on a separate copy stream, so the next swe_step computes while it crosses PCIe.  The host buffers
+ * belong to the library until swe_wait_state returns: their contents are undefined before, and they must stay
+ * allocated.  Pinned (page-locked) buffers are needed for the overlap; pageable ones give a correct, synchronous
+ * copy.  With two snapshots in flight, the next call first waits (on the device) for the older one's copy.
+ * Contexts of a multi-rank or in-process partition take the synchronous swe_get_state path. */
+int swe_get_state_async(swe_ctx *ctx, double *h, double *hu, double *hv);
+
+/* Wait until every swe_get_state_async copy of this context has reached the host. */
+int swe_wait_state(swe_ctx *ctx);
+
 /* Dirichlet boundary data (reading A7''; P:355 sets "Dirichlet boundary conditions ... to the exact
  * solution").  A boundary face whose two vertices are both tagged 2 in swe_mesh.vbc is a Dirichlet face:
  * its ghost state is the trace of the nodal state given here ([nelems*Np] each, caller layout; only the

@@ -25,7 +25,8 @@ EXPORTED = ["swe_nodes", "swe_create", "swe_set_state", "swe_step", "swe_get_sta
             "swe_get_connectivity", "swe_get_info", "swe_last_error", "swe_profile", "swe_profile_read",
             "swe_nccl_unique_id", "swe_link_group", "swe_step_group",
             "swe_host_refel", "swe_host_connectivity", "swe_host_hk", "swe_host_levels", "swe_host_tvb_geometry",
-            "swe_host_halo_plan", "swe_get_decisions", "swe_ipc_handle", "swe_ipc_open", "swe_set_boundary_state"]
+            "swe_host_halo_plan", "swe_get_decisions", "swe_ipc_handle", "swe_ipc_open", "swe_set_boundary_state",
+            "swe_get_state_async", "swe_wait_state"]
 
 
 class SweError(RuntimeError):
@@ -86,6 +87,8 @@ def lib():
         L.swe_set_boundary_state.argtypes = [vp, dp, dp, dp]
         L.swe_regroup.argtypes = [vp]
         L.swe_get_state.argtypes = [vp, dp, dp, dp]
+        L.swe_get_state_async.argtypes = [vp, dp, dp, dp]
+        L.swe_wait_state.argtypes = [vp]
         L.swe_destroy.argtypes = [vp]
         L.swe_destroy.restype = None
         L.swe_get_levels.argtypes = [vp, ip]
@@ -349,6 +352,17 @@ class Solver:
         """Write into caller-provided (e.g. pinned) contiguous float64 buffers of K*Np elements."""
         h, hu, hv = self._out(h), self._out(hu), self._out(hv)
         _check(lib().swe_get_state(self._h, _p(h), _p(hu), _p(hv)), self._h)
+
+    def get_state_async(self, h, hu, hv):
+        """Enqueue a copy of the current state into h, hu, hv (pinned for overlap) and return at once; the buffers
+        hold the state after wait_state().  The solver keeps references to them until then."""
+        h, hu, hv = self._out(h), self._out(hu), self._out(hv)
+        self._pending = getattr(self, "_pending", []) + [(h, hu, hv)]
+        _check(lib().swe_get_state_async(self._h, _p(h), _p(hu), _p(hv)), self._h)
+
+    def wait_state(self):
+        _check(lib().swe_wait_state(self._h), self._h)
+        self._pending = []
 
     def levels(self):
         a = np.zeros(self.K, dtype=np.int32)

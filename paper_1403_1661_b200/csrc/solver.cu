@@ -176,6 +176,41 @@ struct GatherParams {
   const void *Q;  // T-typed internal state
   double *h, *hu, *hv;
 };
+// Caller-layout read-back through a shared tile: a block reads kGatherTile consecutive internal elements' nodes
+// coalesced from the element-blocked state and writes each element's Np consecutive doubles with consecutive lanes
+// (the one-thread-per-element gather below scattered 8-byte stores over 32 caller rows per instruction).
+constexpr int kGatherTile = 128;
+template <typename T>
+__global__ void __launch_bounds__(kGatherTile) k_gather_tile(const __grid_constant__ GatherParams p) {
+  extern __shared__ double tile[];  // [kGatherTile][Np]
+  __shared__ int par_of[kGatherTile], dst_of[kGatherTile];
+  const int k0 = (int)blockIdx.x * kGatherTile, n = min(kGatherTile, p.K - k0), Np = p.Np;
+  const size_t K = p.Kstride;
+  if ((int)threadIdx.x < n) {
+    const int k = k0 + (int)threadIdx.x;
+    int c = 0;
+    for (int l = 1; l < p.nlev; l++) c += (k >= p.off[l]) ? 1 : 0;
+    par_of[threadIdx.x] = p.par[c];
+    dst_of[threadIdx.x] = p.orig[k];
+  }
+  __syncthreads();
+  double *outs[3] = {p.h, p.hu, p.hv};
+  for (int f = 0; f < 3; f++) {
+    for (int idx = (int)threadIdx.x; idx < n * Np; idx += kGatherTile) {  // coalesced reads: element fastest
+      const int el = idx % n, node = idx / n, k = k0 + el;
+      const T *Q = (const T *)p.Q + (size_t)par_of[el] * 3 * Np * eb_pad(K);
+      tile[el * Np + node] = (double)Q[eb_at(k, f * Np + node, 3 * Np)];
+    }
+    __syncthreads();
+    double *out = outs[f];
+    for (int idx = (int)threadIdx.x; idx < n * Np; idx += kGatherTile) {  // row-contiguous writes: node fastest
+      const int el = idx / Np, node = idx % Np;
+      out[(size_t)dst_of[el] * Np + node] = tile[idx];
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T>
 __global__ void k_gather_state(const __grid_constant__ GatherParams p) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -276,6 +311,10 @@ struct Ctx {
   unsigned int *dK2cnt = nullptr;     // [2] list lengths
   long k2u = 0;                       // list-mode updates so far (the slot of an update is k2u & 1)
   double *dGather = nullptr;             // caller-layout state for swe_get_state (allocated on first use)
+  double *dSnap[2] = {nullptr, nullptr};  // swe_get_state_async snapshot buffers (allocated on first use)
+  cudaStream_t ostream = nullptr;         // swe_get_state_async device->host copies
+  cudaEvent_t oevG[2] = {nullptr, nullptr}, oevC[2] = {nullptr, nullptr};  // snapshot gathered / copied
+  long nsnap = 0;                         // swe_get_state_async calls so far
   double *dBndStage = nullptr;           // Dirichlet boundary state, caller layout [3][Kin][Np] (A7'')
   double *dQbnd = nullptr, *dBmean = nullptr;  // ... in the internal layout, and its cell means
   bool bnd_set = false;
@@ -2061,9 +2100,9 @@ int swe_get_state(swe_ctx *h, double *hh, double *hu, double *hv) {
   double *tmp = c->dGather;
   GatherParams g = gather_params(c, tmp, tmp + KNp, tmp + 2 * KNp);
   if (c->f32)
-    k_gather_state<float><<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
+    k_gather_tile<float><<<(c->kown + kGatherTile - 1) / kGatherTile, kGatherTile, sizeof(double) * kGatherTile * c->Np, c->stream>>>(g);
   else
-    k_gather_state<double><<<(c->kown + 127) / 128, 128, 0, c->stream>>>(g);
+    k_gather_tile<double><<<(c->kown + kGatherTile - 1) / kGatherTile, kGatherTile, sizeof(double) * kGatherTile * c->Np, c->stream>>>(g);
   cudaError_t e = cudaGetLastError();
   if (c->kown == c->Kin) {  // every element owned: straight copies
     if (e == cudaSuccess) e = cudaMemcpyAsync(hh, tmp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->stream);
@@ -2088,10 +2127,67 @@ int swe_get_state(swe_ctx *h, double *hh, double *hu, double *hv) {
   return SWE_OK;
 }
 
+int swe_get_state_async(swe_ctx *h, double *hh, double *hu, double *hv) {
+  if (!h || !hh || !hu || !hv) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  if (!c->have_state) return SWE_ERR_STATE;
+  if (c->nranks > 1 || !c->group.empty() || c->kown != c->Kin) return swe_get_state(h, hh, hu, hv);
+  std::vector<Ctx *> G = {c};
+  if (int rc = ensure_materialized_group(G)) return rc;
+  const size_t KNp = (size_t)c->Kin * c->Np;
+  const int i = (int)(c->nsnap & 1);
+  if (!c->ostream) {
+    CK(cudaStreamCreateWithFlags(&c->ostream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; k++) {
+      CK(cudaEventCreateWithFlags(&c->oevG[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->oevC[k], cudaEventDisableTiming));
+    }
+  }
+  if (!c->dSnap[i]) {
+    c->dSnap[i] = (double *)c->dalloc(sizeof(double) * 3 * KNp);
+    if (!c->dSnap[i]) {
+      c->alloc_ok = true;  // a later call may retry
+      c->err = "swe_get_state_async: device allocation failed";
+      return SWE_ERR_NOMEM;
+    }
+  }
+  double *tmp = c->dSnap[i];
+  if (c->nsnap >= 2) CK(cudaStreamWaitEvent(c->stream, c->oevC[i], 0));  // the buffer's previous copy is done
+  GatherParams g = gather_params(c, tmp, tmp + KNp, tmp + 2 * KNp);
+  if (c->f32)
+    k_gather_tile<float><<<(c->kown + kGatherTile - 1) / kGatherTile, kGatherTile, sizeof(double) * kGatherTile * c->Np, c->stream>>>(g);
+  else
+    k_gather_tile<double><<<(c->kown + kGatherTile - 1) / kGatherTile, kGatherTile, sizeof(double) * kGatherTile * c->Np, c->stream>>>(g);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->oevG[i], c->stream));
+  CK(cudaStreamWaitEvent(c->ostream, c->oevG[i], 0));
+  double *outs[3] = {hh, hu, hv};
+  for (int f = 0; f < 3; f++)
+    CK(cudaMemcpyAsync(outs[f], tmp + (size_t)f * KNp, sizeof(double) * KNp, cudaMemcpyDeviceToHost, c->ostream));
+  CK(cudaEventRecord(c->oevC[i], c->ostream));
+  c->nsnap++;
+  return SWE_OK;
+}
+
+int swe_wait_state(swe_ctx *h) {
+  if (!h) return SWE_ERR_ARG;
+  Ctx *c = &h->c;
+  if (c->ostream) CK(cudaStreamSynchronize(c->ostream));
+  return SWE_OK;
+}
+
 void swe_destroy(swe_ctx *h) {
   if (!h) return;
   Ctx *c = &h->c;
   if (c->stream || c->dQ) cudaStreamSynchronize(c->stream);
+  if (c->ostream) {
+    cudaStreamSynchronize(c->ostream);
+    cudaStreamDestroy(c->ostream);
+    for (int k = 0; k < 2; k++) {
+      if (c->oevG[k]) cudaEventDestroy(c->oevG[k]);
+      if (c->oevC[k]) cudaEventDestroy(c->oevC[k]);
+    }
+  }
   if (c->cstream) {
     cudaStreamSynchronize(c->cstream);
     cudaStreamDestroy(c->cstream);
@@ -2110,7 +2206,8 @@ void swe_destroy(swe_ctx *h) {
   void *ptrs[] = {c->dQ,       c->dR,     c->dB,    c->dV,        c->dMeans,   c->dUT,    c->dTalpha, c->dTgeo, c->dGeo,
                   c->dAe,      c->dStage, c->dInjected, c->dWm2,  c->dBcaller, c->dPartials, c->dOpsG, c->dOpsGf, c->dHk, c->dLev, c->dLevRes, c->dFlag,
                   c->dRmin,    c->dXsBuf, c->dXrBuf, c->dE2E,     c->dTcode,   c->dOrig,  c->dXidx,
-                  c->dDry,   c->dCounters, c->dGather, c->dDec, c->dBndStage, c->dQbnd, c->dBmean, c->dK2list, c->dK2cnt};
+                  c->dDry,   c->dCounters, c->dGather, c->dDec, c->dBndStage, c->dQbnd, c->dBmean, c->dK2list, c->dK2cnt,
+                  c->dSnap[0], c->dSnap[1]};
   clear_graphs(c);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->gev0) cudaEventDestroy(c->gev0);

@@ -270,6 +270,37 @@ def test_tensor_path_is_run_to_run_bit_identical(N):
         assert np.array_equal(a, b)
 
 
+def test_get_state_async_matches_synchronous_reads():
+    """swe_get_state_async (snapshot gathered on the device, D2H on a copy stream while the next steps run; two
+    snapshot buffers) delivers, after swe_wait_state, exactly the state swe_get_state reads at the same point --
+    also with three snapshots in flight, where the third waits for the first buffer's copy."""
+    import torch
+    w = si.c4_dambreak(N=3, base=5)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    m = w.mesh
+    x, y = P.nodes(m.vx, m.vy, m.etov, 3)
+    B, h, hu, hv = w.fields(x, y)
+    ref = []
+    s = P.Solver(m.vx, m.vy, m.etov, B, 3, w.g, params=w.params)
+    s.set_state(h, hu, hv)
+    for _ in range(4):
+        s.step(dt, 3)
+        ref.append(s.get_state())
+    s.close()
+    pin = lambda: torch.zeros(h.shape, dtype=torch.float64).pin_memory().numpy()  # noqa: E731
+    outs = [tuple(pin() for _ in range(3)) for _ in range(4)]
+    s = P.Solver(m.vx, m.vy, m.etov, B, 3, w.g, params=w.params)
+    s.set_state(h, hu, hv)
+    for k in range(4):
+        s.step(dt, 3)
+        s.get_state_async(*outs[k])
+    s.wait_state()
+    s.close()
+    for k in range(4):
+        for a, b in zip(outs[k], ref[k]):
+            assert np.array_equal(a, b), k
+
+
 def test_convergence_sweep_n1_to_n5_through_the_abi():
     """C2 (BASELINE configs[1]): the translating vortex on periodic meshes 2 x n x n,
     n = 16, 32, 64, N = 1..5, through the C ABI; the L2 error of h converges at least like
