@@ -82,16 +82,30 @@ __global__ void k_levels(int K, const double *hk, const double *ae, const double
 }
 
 // caller layout [K][Np] (3 arrays) -> internal element-blocked [K/32][3][Np][32] in internal order
+// Through a shared tile, as k_gather_tile: each caller row (Np consecutive doubles) is read by consecutive lanes,
+// each element-blocked row written by consecutive lanes.  Launch: blocks of kScatterTile threads, dynamic shared
+// memory kScatterTile * Np doubles.
+constexpr int kScatterTile = 128;
 template <typename T>
-__global__ void k_scatter_state(int K, int Np, const int *orig, const double *h, const double *hu, const double *hv,
-                                T *Q) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  size_t e = (size_t)orig[k];
-  for (int i = 0; i < Np; i++) {
-    Q[eb_at(k, i, 3 * Np)] = (T)h[e * Np + i];
-    Q[eb_at(k, Np + i, 3 * Np)] = (T)hu[e * Np + i];
-    Q[eb_at(k, 2 * Np + i, 3 * Np)] = (T)hv[e * Np + i];
+__global__ void __launch_bounds__(kScatterTile) k_scatter_state(int K, int Np, const int *orig, const double *h,
+                                                                const double *hu, const double *hv, T *Q) {
+  extern __shared__ double tile[];  // [kScatterTile][Np]
+  __shared__ int src_of[kScatterTile];
+  const int k0 = (int)blockIdx.x * kScatterTile, n = min(kScatterTile, K - k0);
+  if ((int)threadIdx.x < n) src_of[threadIdx.x] = orig[k0 + (int)threadIdx.x];
+  __syncthreads();
+  const double *ins[3] = {h, hu, hv};
+  for (int f = 0; f < 3; f++) {
+    for (int idx = (int)threadIdx.x; idx < n * Np; idx += kScatterTile) {  // row-contiguous reads: node fastest
+      const int el = idx / Np, node = idx % Np;
+      tile[idx] = ins[f][(size_t)src_of[el] * Np + node];
+    }
+    __syncthreads();
+    for (int idx = (int)threadIdx.x; idx < n * Np; idx += kScatterTile) {  // coalesced writes: element fastest
+      const int el = idx % n, node = idx / n;
+      Q[eb_at(k0 + el, f * Np + node, 3 * Np)] = (T)tile[el * Np + node];
+    }
+    __syncthreads();
   }
 }
 
@@ -1164,10 +1178,10 @@ static int scatter_bnd(Ctx *c) {
   const size_t KNp = (size_t)c->Kin * c->Np;
   double *st = c->dBndStage;
   if (c->f32) {
-    k_scatter_state<float><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, st, st + KNp, st + 2 * KNp, (float *)c->dQbnd);
+    k_scatter_state<float><<<(K + kScatterTile - 1) / kScatterTile, kScatterTile, sizeof(double) * kScatterTile * c->Np, c->stream>>>(K, c->Np, c->dOrig, st, st + KNp, st + 2 * KNp, (float *)c->dQbnd);
     k_cell_means<float><<<nb, 128, 0, c->stream>>>(K, c->Np, (const float *)c->dQbnd, c->dWm2, (float *)c->dBmean);
   } else {
-    k_scatter_state<double><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, st, st + KNp, st + 2 * KNp, c->dQbnd);
+    k_scatter_state<double><<<(K + kScatterTile - 1) / kScatterTile, kScatterTile, sizeof(double) * kScatterTile * c->Np, c->stream>>>(K, c->Np, c->dOrig, st, st + KNp, st + 2 * KNp, c->dQbnd);
     k_cell_means<double><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dQbnd, c->dWm2, c->dBmean);
   }
   CK(cudaGetLastError());
@@ -1185,13 +1199,12 @@ static int check_bnd(Ctx *c) {
 // dry flags, counters, AB ramp and clocks.
 static int materialize_state(Ctx *c) {
   const int K = c->K;
-  const int nb = (K + 127) / 128;
   const size_t KNp = (size_t)c->Kin * c->Np;
   if (c->f32)
-    k_scatter_state<float><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp,
+    k_scatter_state<float><<<(K + kScatterTile - 1) / kScatterTile, kScatterTile, sizeof(double) * kScatterTile * c->Np, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp,
                                                       c->dStage + 2 * KNp, (float *)c->dQ);
   else
-    k_scatter_state<double><<<nb, 128, 0, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp,
+    k_scatter_state<double><<<(K + kScatterTile - 1) / kScatterTile, kScatterTile, sizeof(double) * kScatterTile * c->Np, c->stream>>>(K, c->Np, c->dOrig, c->dStage, c->dStage + KNp,
                                                        c->dStage + 2 * KNp, c->dQ);
   CK(cudaGetLastError());
   if (int rc = scatter_bnd(c)) return rc;
