@@ -575,8 +575,19 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
     if (smem2 > 48 * 1024)
       cudaFuncSetAttribute(k_rhs_update_mma2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     constexpr int bs = mma2_block<N>();
-    launch_pdl(k_rhs_update_mma2<N>, (n + bs - 1) / bs, bs, smem2, s,
-               reinterpret_cast<const StepParams &>(p));
+    int grid = (n + bs - 1) / bs;
+    if constexpr (N >= K1_MMA2_PERSIST) {
+    static int resident[6] = {0, 0, 0, 0, 0, 0};  // SMs x resident blocks (per order; one device per process)
+    if (!resident[N]) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update_mma2<N>, bs, smem2);
+      resident[N] = std::max(1, sms * per_sm);
+    }
+    grid = std::min(grid, resident[N]);
+    }
+    launch_pdl(k_rhs_update_mma2<N>, grid, bs, smem2, s, reinterpret_cast<const StepParams &>(p));
     return;
   }
 #if K1_CARVEOUT >= 0
