@@ -202,8 +202,8 @@ def _ipc_worker(rank, world, port, outdir, case):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)  # every rank on the one GPU of the box: NCCL refuses this, IPC does not
-    if case == "c4":
-        w = si.c4_dambreak(N=3, base=5)
+    if case.startswith("c4"):  # "c4": N = 3 (scalar K1); "c4n5": N = 5 (the persistent DMMA K1 on sub-ranges)
+        w = si.c4_dambreak(N=5 if case == "c4n5" else 3, base=5)
         m = w.mesh
         owner = _partition(m, world)
         gid = None
@@ -236,7 +236,7 @@ def _ipc_worker(rank, world, port, outdir, case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,world", [("c4", 2), ("c4", 3), ("c5", 2)])
+@pytest.mark.parametrize("case,world", [("c4", 2), ("c4", 3), ("c5", 2), ("c4n5", 2)])
 def test_ipc_ranks_bit_identical(case, world, tmp_path):
     """The CUDA-IPC transport with one process per rank (all on this box's single GPU): boundary-first
     level updates with the halo exchanges on a communication stream (stream-memory-op flags, peer copies
@@ -245,8 +245,8 @@ def test_ipc_ranks_bit_identical(case, world, tmp_path):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     mp.spawn(_ipc_worker, args=(world, _free_port(), str(tmp_path), case), nprocs=world, join=True)
-    if case == "c4":
-        w = si.c4_dambreak(N=3, base=5)
+    if case.startswith("c4"):
+        w = si.c4_dambreak(N=5 if case == "c4n5" else 3, base=5)
         m = w.mesh
         L, nsteps = 3, 6
         dt = si.dt_for(m, w.N, w.g, 1.875, 13.0, 0.2)
