@@ -129,3 +129,24 @@ def test_periodic_vortex_mrab_100_macro_steps():
     dt = si.dt_for(w.mesh, 3, w.g, 1.0, 0.0, 0.1, u_max=2.0)
     io = _replayed_parity(w, 100, dt, 3)
     assert io["levels_used"] == 3
+
+
+def test_c5_fullsize_1000_macro_steps_graph_replay(c5):
+    """The bench's launch configuration (CUDA-graph replay, K2 list pass, one macro step = 15 K1 + 15 K2) run for 1000
+    macro steps (8,000 finest substeps, ~1 minute of simulated time): every step finite (swe_step reports non-finite
+    states), h >= 0 at every node, and mass conserved up to the dry branch's counted injection (Alg. 3, reading A13)."""
+    w, x, y, B, h, hu, hv, dt = c5
+    m = w.mesh
+    s = P.Solver(m.vx, m.vy, m.etov, B, w.N, w.g, params=w.params)
+    s.set_state(h, hu, hv)
+    s.step(dt, w.nlevels)
+    i0 = s.info()
+    for _ in range(999):
+        s.step(dt, w.nlevels)
+    i1 = s.info()
+    assert i1["min_h"] >= 0.0
+    drift = i1["mass"] - i0["mass"] - (i1["injected_mass"] - i0["injected_mass"])
+    assert abs(drift) <= 1e-11 * i0["mass"], (drift, i0["mass"])
+    hh, _, _ = s.get_state()
+    assert np.isfinite(hh).all() and hh.min() >= 0.0
+    s.close()
