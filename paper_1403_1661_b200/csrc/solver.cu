@@ -576,16 +576,16 @@ static void launch_k1(const StepParamsT<T> &p, cudaStream_t s) {
       cudaFuncSetAttribute(k_rhs_update_mma2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     constexpr int bs = mma2_block<N>();
     int grid = (n + bs - 1) / bs;
-    if constexpr (N >= K1_MMA2_PERSIST) {
-    static int resident[6] = {0, 0, 0, 0, 0, 0};  // SMs x resident blocks (per order; one device per process)
-    if (!resident[N]) {
-      int dev = 0, sms = 0, per_sm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update_mma2<N>, bs, smem2);
-      resident[N] = std::max(1, sms * per_sm);
-    }
-    grid = std::min(grid, resident[N]);
+    if constexpr (N >= K1_MMA2_PERSIST) {  // persistent grid: SMs x resident blocks
+      static int resident[6] = {0, 0, 0, 0, 0, 0};  // per order (one device per process)
+      if (!resident[N]) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rhs_update_mma2<N>, bs, smem2);
+        resident[N] = std::max(1, sms * per_sm);
+      }
+      grid = std::min(grid, resident[N]);
     }
     launch_pdl(k_rhs_update_mma2<N>, grid, bs, smem2, s, reinterpret_cast<const StepParams &>(p));
     return;
