@@ -150,3 +150,17 @@ def test_c5_fullsize_1000_macro_steps_graph_replay(c5):
     hh, _, _ = s.get_state()
     assert np.isfinite(hh).all() and hh.min() >= 0.0
     s.close()
+
+
+@pytest.mark.parametrize("N,base", [(4, 1), (5, 2)])
+def test_c4_tensor_path_100_macro_steps(N, base):
+    """North_star's "after 100 steps" bar for the tensor-path K1 (k_rhs_update_mma2): the C4 dam break (3 MRAB
+    levels, wet/dry, PP + TVB) at N = 4 on the full 187,560-triangle mesh and at N = 5 on the base-2 mesh,
+    100 macro steps, element-wise parity with the oracle (decision replay) and equal counters."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    w = si.c4_dambreak(N=N, base=base)
+    dt = si.dt_for(w.mesh, w.N, w.g, 1.875, 13.0, 0.2)
+    io = _replayed_parity(w, 100, dt, 3)
+    assert io["n_pp"] > 0 and io["n_dry"] > 0 and io["levels_used"] == 3
